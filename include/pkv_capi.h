@@ -1,0 +1,181 @@
+/* pkv_capi.h — C ABI of the B200-native ProxyKV pruning hot path
+ * (libpkv_b200.so). Plain pointers and sizes only; no C++ or torch types.
+ *
+ * Path: proxy scoring -> HybridAxialMapper forward -> per-head Top-K select
+ *       -> KV compaction. Each entry point names the reference
+ * interface it replaces (paths relative to /root/reference/).
+ *
+ * Conventions
+ *  - Status codes mirror the reference exception taxonomy
+ *    (proj/include/proxykv/common.hpp:13-52): PKV_ESHAPE <-> ShapeError,
+ *    PKV_EVALUE <-> ValueError, PKV_ECONFIG <-> ConfigError. The message text
+ *    (pkv_last_error, thread-local) mirrors the reference PKV_CHECK text.
+ *  - "_dev" pointers are device pointers owned by the caller; "_host" pointers
+ *    are host memory (pinned or pageable). Device work is stream-ordered on
+ *    the given cudaStream_t (passed as void*; NULL = legacy default stream).
+ *  - One pkv_ctx per host thread, or external synchronisation.
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point returns PKV_ENODEV.
+ */
+#ifndef PKV_CAPI_H
+#define PKV_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PKV_OK = 0,
+    PKV_ESHAPE = 1,  /* ShapeError  */
+    PKV_EVALUE = 2,  /* ValueError  */
+    PKV_ECUDA = 3,   /* CUDA runtime / launch failure */
+    PKV_ENCCL = 4,   /* reserved: collective failure */
+    PKV_ECONFIG = 5, /* ConfigError (incl. configurations the GPU path does not support) */
+    PKV_ENODEV = 6   /* no sm_100 device */
+} pkv_status;
+
+typedef struct pkv_ctx_s* pkv_ctx;
+typedef struct pkv_mapper_s* pkv_mapper;
+typedef struct pkv_pruner_s* pkv_pruner;
+
+/* ---------------------------------------------------------------- runtime */
+int pkv_abi_version(void);
+const char* pkv_last_error(void);
+/* Number of visible CUDA devices with compute capability 10.x (0 on a CPU box). */
+int pkv_sm100_device_count(void);
+pkv_status pkv_ctx_create(int device, pkv_ctx* out);
+void pkv_ctx_destroy(pkv_ctx ctx);
+/* Launches of this library's kernels since ctx creation (for bench accounting). */
+int64_t pkv_ctx_launch_count(pkv_ctx ctx);
+
+/* ------------------------------------------------------- select (a-3) ---- */
+/* Replaces retention_count, proj/src/pruning.cpp:14-18 (pruning.hpp:14):
+ * ceil(rho * n) in double. PKV_EVALUE if rho∉(0,1] or n<=0. */
+pkv_status pkv_retention_count(double rho, int64_t n, int64_t* k_out);
+
+/* Replaces topk_indices + topk_mask (proj/src/pruning.cpp:20-56;
+ * pruning.hpp:18,32) and the index lists of apply_mask (pruning.cpp:197-215;
+ * pruning.hpp:57): for each of `slices` rows of `n` fp32 scores, selects the k
+ * best under v[a] > v[b] || (v[a] == v[b] && a < b) (-0.0 == +0.0), writing
+ * a 0/1 mask [slices, n] and/or the ascending retained indices [slices, k].
+ * Radix select on the GPU; bit-exact with the reference for fp32 scores.
+ * PKV_EVALUE if k∉[1,n]. NaN scores: unspecified (as in the reference). */
+pkv_status pkv_topk_select(pkv_ctx ctx, const float* scores_dev, int64_t slices, int64_t n, int64_t k,
+                           uint8_t* mask_dev, int32_t* idx_asc_dev, void* stream);
+
+/* Host-buffer form of topk_mask (pruning.cpp:37-56): fp64 scores (must be
+ * fp32-representable for bit-exact parity) -> mask bits; H2D/D2H inside. */
+pkv_status pkv_topk_mask_host(pkv_ctx ctx, const double* scores_host, int64_t slices, int64_t n, double rho,
+                              uint8_t* bits_host, int64_t* k_out);
+
+/* --------------------------------------------------- compaction (a-4) ---- */
+/* Packed KV gather in apply_mask order (no reference code; the reference only
+ * reports indices, pruning.cpp:197-215): for s < slices, j < k,
+ *   k_out[s, j, :] = k_in[s, idx_asc[s, j], :]   (same for V)
+ * rows of d elements of elem_bytes (2 for bf16/fp16). 128-bit vectorised. */
+pkv_status pkv_compact_kv(pkv_ctx ctx, const void* k_in_dev, const void* v_in_dev, const int32_t* idx_asc_dev,
+                          int64_t slices, int64_t n, int64_t k, int64_t d, int64_t elem_bytes, void* k_out_dev,
+                          void* v_out_dev, void* stream);
+
+/* ------------------------------------------------------ scoring (a-1) ---- */
+#define PKV_SCORE_REDUCE_MAX 0u /* north star: max over queries (and GQA group) */
+#define PKV_SCORE_REDUCE_SUM 1u /* SPEC.md:423-431 accumulate_attention / PAPER.md:46 */
+#define PKV_SCORE_CAUSAL 2u     /* mask keys j > q + (Nk - Nq) */
+
+/* Proxy reconstruction-importance scoring (SPEC.md:423-431 accumulate_attention,
+ * without materialising attn[B,H,Nq,Nk]):
+ *   P[l,h,q,:] = softmax(Q[l,h,q]·K[l,h/g,:]^T / sqrt(d)),  g = Hq / Hkv
+ *   X[l,kh,j]  = max (or sum) over h in group kh and q of P[l,h,q,j]
+ * q_dev bf16 [L, Hq, Nq, d], k_dev bf16 [L, Hkv, Nk, d], x_out fp32 [L, Hkv, Nk].
+ * lse_dev (nullable) fp32 [L, Hq, Nq]: natural-log row LSE of the scaled
+ * scores, e.g. from the proxy's own prefill; when NULL a first tensor-core
+ * pass computes it. d must be 64 or 128. */
+pkv_status pkv_score(pkv_ctx ctx, const void* q_dev, const void* k_dev, int64_t L, int64_t Hq, int64_t Hkv,
+                     int64_t Nq, int64_t Nk, int64_t d, uint32_t flags, const float* lse_dev, float* x_out_dev,
+                     void* stream);
+
+/* Pass 1 alone: lse_out fp32 [L, Hq, Nq]. */
+pkv_status pkv_score_lse(pkv_ctx ctx, const void* q_dev, const void* k_dev, int64_t L, int64_t Hq, int64_t Hkv,
+                         int64_t Nq, int64_t Nk, int64_t d, uint32_t flags, float* lse_out_dev, void* stream);
+
+/* ------------------------------------------------------- mapper (a-2) ---- */
+/* geom5 = {target_layers, target_heads, proxy_layers, proxy_heads, head_dim}
+ *   (ModelGeometry, proj/include/proxykv/mapper.hpp:16-25)
+ * cfg12 = {d_time, encoder_layers, encoder_heads, ffn_mult, d_head, crop_len,
+ *          stride, synthetic_heads, stage_conv, stage_encoder, stage_cross,
+ *          normalize_input}   stage_*: 0 active, 1 bypass
+ *   (MapperConfig, mapper.hpp:35-55) */
+
+/* Replaces layer_pair, proj/src/mapper.cpp:44-49 (mapper.hpp:58). */
+pkv_status pkv_layer_pair(int64_t target_layer, const int64_t* geom5, int64_t* proxy_layer_out);
+/* Replaces window_offsets, proj/src/mapper.cpp:66-79 (mapper.hpp:65). */
+pkv_status pkv_window_offsets(int64_t n, int64_t crop, int64_t stride, int64_t* out, int64_t cap,
+                              int64_t* count_out);
+/* Replaces MapperParams::init, proj/src/mapper.cpp:97-164 (mapper.hpp:94):
+ * the reference initialisation as a flat fp64 blob in named_parameters() then
+ * named_buffers() order (mapper.cpp:166-225). blob_out may be NULL to query
+ * the count. */
+pkv_status pkv_mapper_init_params(const int64_t* geom5, const int64_t* cfg12, uint64_t seed, double* blob_out,
+                                  int64_t* count_out);
+
+#define PKV_MAPPER_FP16 1u   /* fp16 operands, fp32 accumulate (1 MMA per product) */
+#define PKV_MAPPER_FP16X2 2u /* activations split hi+lo fp16 (2 MMAs per product) */
+#define PKV_MAPPER_FP16X3 3u /* activations and weights split (3 MMAs per product) */
+
+/* Uploads a mapper (weights in the pkv_mapper_init_params layout, fp64) to the
+ * device; prepares the B200 weight layouts (K-major fp16 planes, BN folded,
+ * stage-3 query/out projections folded). */
+pkv_status pkv_mapper_create(pkv_ctx ctx, const int64_t* geom5, const int64_t* cfg12, const double* blob,
+                             int64_t count, uint32_t precision, pkv_mapper* out);
+void pkv_mapper_destroy(pkv_mapper m);
+
+/* Replaces forward_full, proj/src/mapper.cpp:379-398 (mapper.hpp:126), eval
+ * mode: x_all fp32 [B, L_s, H_s, N] -> y_all fp32 [B, L_l, H_l, N] (raw
+ * logits). Includes sliding_forward's window overlap average
+ * (mapper.cpp:344-377); shared proxy layers are computed once. */
+pkv_status pkv_mapper_forward_full(pkv_mapper m, const float* x_all_dev, int64_t B, int64_t N, float* y_all_dev,
+                                   void* stream);
+/* Replaces sliding_forward (mapper.cpp:344-377; forward_pair when N <= crop):
+ * x fp32 [B, H_s, N] -> y fp32 [B, H_l, N]. */
+pkv_status pkv_mapper_sliding_forward(pkv_mapper m, const float* x_dev, int64_t B, int64_t N, float* y_dev,
+                                      void* stream);
+
+/* ------------------------------------------------- whole path (a-1..a-4) -- */
+/* A pruner owns the workspaces for one context shape:
+ *   proxy: L_s layers, Hq query heads, H_s KV heads, head dim dp
+ *   target: L_l layers, H_l KV heads, head dim dt; context N; ratio rho. */
+pkv_status pkv_pruner_create(pkv_ctx ctx, pkv_mapper m, int64_t Hq, int64_t dp, int64_t dt, int64_t N, double rho,
+                             uint32_t score_flags, pkv_pruner* out);
+void pkv_pruner_destroy(pkv_pruner p);
+/* K = retention_count(rho, N) for this pruner. */
+int64_t pkv_pruner_k(pkv_pruner p);
+/* score -> map -> select -> compact, device buffers:
+ *   q bf16 [L_s, Hq, N, dp], kp bf16 [L_s, H_s, N, dp] (proxy),
+ *   kt, vt bf16/fp16 [L_l, H_l, N, dt] (target KV),
+ *   k_out, v_out [L_l, H_l, K, dt], idx_out int32 [L_l, H_l, K] (nullable),
+ *   scores_out fp32 [L_l, H_l, N] (nullable: mapped scores Ŷ). */
+pkv_status pkv_pruner_run(pkv_pruner p, const void* q_dev, const void* kp_dev, const void* kt_dev,
+                          const void* vt_dev, void* k_out_dev, void* v_out_dev, int32_t* idx_out_dev,
+                          float* scores_out_dev, void* stream);
+/* Same with host buffers: H2D of the inputs and D2H of the outputs are part
+ * of the call (the reference-facing end-to-end form). */
+pkv_status pkv_pruner_run_host(pkv_pruner p, const void* q_host, const void* kp_host, const void* kt_host,
+                               const void* vt_host, void* k_out_host, void* v_out_host, int32_t* idx_out_host,
+                               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#endif /* PKV_CAPI_H */

@@ -1,0 +1,248 @@
+// C-ABI harness over the UNMODIFIED reference C++ API (/root/reference/proj),
+// compiled together with the reference sources into oracle/_ref/libpkvref.so
+// by oracle/Makefile. TEST INFRASTRUCTURE ONLY: imported by tests/, by
+// __graft_entry__.smoke() as the checker, and by bench.py's cpu_baseline /
+// --impl reference legs. The product path never links or loads this.
+//
+// Every entry point forwards to the reference function named in its comment
+// and converts C++ exceptions into status codes:
+//   0 ok, 1 ShapeError, 2 ValueError, 5 ConfigError, 9 other.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "proxykv/common.hpp"
+#include "proxykv/mapper.hpp"
+#include "proxykv/pruning.hpp"
+#include "proxykv/rng.hpp"
+#include "proxykv/tensor.hpp"
+
+using namespace proxykv;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const ShapeError& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const ValueError& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const ConfigError& e) {
+        g_err = e.what();
+        return 5;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 9;
+    }
+}
+
+Tensor make_tensor(const double* data, const int64_t* shape, int rank) {
+    Shape s(shape, shape + rank);
+    std::vector<double> v(static_cast<size_t>(shape_numel(s)));
+    std::memcpy(v.data(), data, v.size() * sizeof(double));
+    return Tensor::from_data(s, std::move(v));
+}
+
+struct RefMapper {
+    MapperParams params;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* pkvref_last_error() { return g_err.c_str(); }
+
+// pruning.cpp:14-18
+int pkvref_retention_count(double rho, int64_t n, int64_t* out) {
+    return guard([&] { *out = retention_count(rho, n); });
+}
+
+// pruning.cpp:20-35 (indices come back in nth_element order, unsorted)
+int pkvref_topk_indices(const double* values, int64_t n, int64_t k, int64_t* out) {
+    return guard([&] {
+        const auto idx = topk_indices(values, n, k);
+        std::memcpy(out, idx.data(), idx.size() * sizeof(int64_t));
+    });
+}
+
+// pruning.cpp:37-56 — scores of arbitrary rank; bits_out has numel entries.
+int pkvref_topk_mask(const double* scores, const int64_t* shape, int rank, double rho,
+                     uint8_t* bits_out, int64_t* k_out) {
+    return guard([&] {
+        const PruneMask m = topk_mask(make_tensor(scores, shape, rank), rho);
+        std::memcpy(bits_out, m.bits.data(), m.bits.size());
+        *k_out = m.k;
+    });
+}
+
+// pruning.cpp:197-215 — retained indices per slice (ascending), [slices, k].
+int pkvref_apply_mask(const uint8_t* bits, const int64_t* shape, int rank, int64_t k,
+                      int64_t head_dim, int64_t bytes_per_elem, int64_t* idx_out,
+                      int64_t* dropped_per_slice, int64_t* bytes_saved_per_head,
+                      int64_t* bytes_saved_total) {
+    return guard([&] {
+        PruneMask m;
+        m.shape = Shape(shape, shape + rank);
+        m.bits.assign(bits, bits + shape_numel(m.shape));
+        m.k = k;
+        const MaskApplication app = apply_mask(m, head_dim, bytes_per_elem);
+        int64_t off = 0;
+        for (const auto& list : app.retained) {
+            std::memcpy(idx_out + off, list.data(), list.size() * sizeof(int64_t));
+            off += static_cast<int64_t>(list.size());
+        }
+        *dropped_per_slice = app.dropped_per_slice;
+        *bytes_saved_per_head = app.bytes_saved_per_head;
+        *bytes_saved_total = app.bytes_saved_total;
+    });
+}
+
+// pruning.cpp:91-117
+int pkvref_topk_overlap_per_slice(const uint8_t* a, const uint8_t* b, const int64_t* shape,
+                                  int rank, int64_t ka, int64_t kb, double* out) {
+    return guard([&] {
+        PruneMask ma, mb;
+        ma.shape = mb.shape = Shape(shape, shape + rank);
+        ma.bits.assign(a, a + shape_numel(ma.shape));
+        mb.bits.assign(b, b + shape_numel(mb.shape));
+        ma.k = ka;
+        mb.k = kb;
+        const auto v = topk_overlap_per_slice(ma, mb);
+        std::memcpy(out, v.data(), v.size() * sizeof(double));
+    });
+}
+
+// mapper.cpp:44-49
+int pkvref_layer_pair(int64_t target_layer, const int64_t* geom5, int64_t* out) {
+    return guard([&] {
+        ModelGeometry g{geom5[0], geom5[1], geom5[2], geom5[3], geom5[4]};
+        *out = layer_pair(target_layer, g);
+    });
+}
+
+// mapper.cpp:66-79 — writes up to cap offsets, returns count in *count.
+int pkvref_window_offsets(int64_t n, int64_t crop, int64_t stride, int64_t* out, int64_t cap,
+                          int64_t* count) {
+    return guard([&] {
+        const auto v = window_offsets(n, crop, stride);
+        *count = static_cast<int64_t>(v.size());
+        for (size_t i = 0; i < v.size() && static_cast<int64_t>(i) < cap; ++i) {
+            out[i] = v[i];
+        }
+    });
+}
+
+// mapper.cpp:51-64
+int pkvref_sinusoidal_pe(int64_t n, int64_t d_time, double* out) {
+    return guard([&] {
+        const Tensor pe = sinusoidal_pe(n, d_time);
+        std::memcpy(out, pe.data().data(), pe.data().size() * sizeof(double));
+    });
+}
+
+// MapperParams::init mapper.cpp:97-164.
+// geom5 = {target_layers, target_heads, proxy_layers, proxy_heads, head_dim}
+// cfg   = {d_time, encoder_layers, encoder_heads, ffn_mult, d_head, crop_len,
+//          stride, synthetic_heads, stage_conv, stage_encoder, stage_cross,
+//          normalize_input}   (stage: 0 active, 1 bypass)
+int pkvref_mapper_create(const int64_t* geom5, const int64_t* cfg12, uint64_t seed, void** out) {
+    return guard([&] {
+        ModelGeometry g{geom5[0], geom5[1], geom5[2], geom5[3], geom5[4]};
+        MapperConfig c;
+        c.d_time = cfg12[0];
+        c.encoder_layers = cfg12[1];
+        c.encoder_heads = cfg12[2];
+        c.ffn_mult = cfg12[3];
+        c.d_head = cfg12[4];
+        c.crop_len = cfg12[5];
+        c.stride = cfg12[6];
+        c.synthetic_heads = cfg12[7];
+        c.stage_conv = cfg12[8] ? StageMode::kBypass : StageMode::kActive;
+        c.stage_encoder = cfg12[9] ? StageMode::kBypass : StageMode::kActive;
+        c.stage_cross = cfg12[10] ? StageMode::kBypass : StageMode::kActive;
+        c.normalize_input = cfg12[11] != 0;
+        auto* m = new RefMapper{MapperParams::init(g, c, seed)};
+        m->params.set_trainable(false);
+        *out = m;
+    });
+}
+
+void pkvref_mapper_destroy(void* h) { delete static_cast<RefMapper*>(h); }
+
+// named_parameters() then named_buffers() (mapper.cpp:166-225): number of
+// tensors, and for tensor i its name / numel / flat fp64 values.
+int pkvref_mapper_tensor_count(void* h) {
+    auto& p = static_cast<RefMapper*>(h)->params;
+    return static_cast<int>(p.named_parameters().size() + p.named_buffers().size());
+}
+
+int pkvref_mapper_tensor(void* h, int i, char* name, int name_cap, int64_t* shape, int* rank,
+                         double* values /* nullable */) {
+    return guard([&] {
+        auto& p = static_cast<RefMapper*>(h)->params;
+        auto all = p.named_parameters();
+        for (auto& b : p.named_buffers()) {
+            all.push_back(b);
+        }
+        const auto& [n, t] = all.at(static_cast<size_t>(i));
+        std::snprintf(name, static_cast<size_t>(name_cap), "%s", n.c_str());
+        *rank = static_cast<int>(t.shape().size());
+        for (size_t d = 0; d < t.shape().size(); ++d) {
+            shape[d] = t.shape()[d];
+        }
+        if (values) {
+            std::memcpy(values, t.data().data(), t.data().size() * sizeof(double));
+        }
+    });
+}
+
+// mapper.cpp:274-342, eval mode. x [B, H_s, n] -> out [B, H_l, n].
+int pkvref_forward_pair(void* h, const double* x, int64_t b, int64_t hs, int64_t n, double* out) {
+    return guard([&] {
+        auto& p = static_cast<RefMapper*>(h)->params;
+        const int64_t shape[3] = {b, hs, n};
+        const Tensor y = forward_pair(make_tensor(x, shape, 3), p, false);
+        std::memcpy(out, y.data().data(), y.data().size() * sizeof(double));
+    });
+}
+
+// mapper.cpp:344-377
+int pkvref_sliding_forward(void* h, const double* x, int64_t b, int64_t hs, int64_t n, double* out) {
+    return guard([&] {
+        auto& p = static_cast<RefMapper*>(h)->params;
+        const int64_t shape[3] = {b, hs, n};
+        const Tensor y = sliding_forward(make_tensor(x, shape, 3), p);
+        std::memcpy(out, y.data().data(), y.data().size() * sizeof(double));
+    });
+}
+
+// mapper.cpp:379-398. x_all [B, L_s, H_s, N] -> out [B, L_l, H_l, N].
+int pkvref_forward_full(void* h, const double* x, int64_t b, int64_t ls, int64_t hs, int64_t n,
+                        double* out) {
+    return guard([&] {
+        auto& p = static_cast<RefMapper*>(h)->params;
+        const int64_t shape[4] = {b, ls, hs, n};
+        const Tensor y = forward_full(make_tensor(x, shape, 4), p);
+        std::memcpy(out, y.data().data(), y.data().size() * sizeof(double));
+    });
+}
+
+// The reference's own Rng (rng.hpp:25-87), for regenerating the test inputs
+// of test_pruning.cpp / test_mapper.cpp in the golden-vector script.
+void* pkvref_rng_create(uint64_t seed) { return new Rng(seed); }
+void pkvref_rng_destroy(void* h) { delete static_cast<Rng*>(h); }
+double pkvref_rng_uniform(void* h, double lo, double hi) { return static_cast<Rng*>(h)->uniform(lo, hi); }
+uint64_t pkvref_rng_below(void* h, uint64_t n) { return static_cast<Rng*>(h)->below(n); }
+double pkvref_rng_normal(void* h) { return static_cast<Rng*>(h)->normal(); }
+
+}  // extern "C"

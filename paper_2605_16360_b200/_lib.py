@@ -1,0 +1,103 @@
+"""ctypes binding of libpkv_b200.so (include/pkv_capi.h).
+
+This is exactly the binding a reference-side maintainer would add
+(INTEGRATION.md): plain pointers and sizes, status codes mapped onto the
+reference exception taxonomy (proj/include/proxykv/common.hpp:13-52).
+The library is loaded from the package directory (built in-tree by
+``__graft_entry__.build()``); a missing library is an error, never a fallback.
+"""
+from __future__ import annotations
+
+import builtins
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpkv_b200.so")
+
+
+class PkvError(RuntimeError):
+    """proxykv::Error (common.hpp:13)."""
+
+
+class ShapeError(PkvError):
+    """proxykv::ShapeError (common.hpp:17)."""
+
+
+class PkvValueError(PkvError, builtins.ValueError):
+    """proxykv::ValueError (common.hpp:21)."""
+
+
+class ConfigError(PkvError):
+    """proxykv::ConfigError (common.hpp:29)."""
+
+
+class CudaError(PkvError):
+    """CUDA runtime / launch failure inside the B200 path."""
+
+
+class NoDeviceError(PkvError):
+    """No sm_100 device: the B200 path has no CPU fallback."""
+
+
+_STATUS = {1: ShapeError, 2: PkvValueError, 3: CudaError, 4: CudaError, 5: ConfigError, 6: NoDeviceError}
+
+_c_i64 = ctypes.c_int64
+_c_i64p = ctypes.POINTER(ctypes.c_int64)
+_c_vp = ctypes.c_void_p
+_c_u32 = ctypes.c_uint32
+_c_dbl = ctypes.c_double
+
+# name -> (restype, argtypes). Every symbol include/pkv_capi.h declares.
+SIGNATURES = {
+    "pkv_abi_version": (ctypes.c_int, []),
+    "pkv_last_error": (ctypes.c_char_p, []),
+    "pkv_sm100_device_count": (ctypes.c_int, []),
+    "pkv_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_c_vp)]),
+    "pkv_ctx_destroy": (None, [_c_vp]),
+    "pkv_ctx_launch_count": (_c_i64, [_c_vp]),
+    "pkv_retention_count": (ctypes.c_int, [_c_dbl, _c_i64, _c_i64p]),
+    "pkv_topk_select": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp]),
+    "pkv_topk_mask_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_dbl, _c_vp, _c_i64p]),
+    "pkv_compact_kv": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_vp,
+                                      _c_vp, _c_vp]),
+    "pkv_score": (ctypes.c_int, [_c_vp, _c_vp, _c_vp] + [_c_i64] * 6 + [_c_u32, _c_vp, _c_vp, _c_vp]),
+    "pkv_score_lse": (ctypes.c_int, [_c_vp, _c_vp, _c_vp] + [_c_i64] * 6 + [_c_u32, _c_vp, _c_vp]),
+    "pkv_layer_pair": (ctypes.c_int, [_c_i64, _c_i64p, _c_i64p]),
+    "pkv_window_offsets": (ctypes.c_int, [_c_i64, _c_i64, _c_i64, _c_i64p, _c_i64, _c_i64p]),
+    "pkv_mapper_init_params": (ctypes.c_int, [_c_i64p, _c_i64p, ctypes.c_uint64, _c_vp, _c_i64p]),
+    "pkv_mapper_create": (ctypes.c_int, [_c_vp, _c_i64p, _c_i64p, _c_vp, _c_i64, _c_u32, ctypes.POINTER(_c_vp)]),
+    "pkv_mapper_destroy": (None, [_c_vp]),
+    "pkv_mapper_forward_full": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_vp, _c_vp]),
+    "pkv_mapper_sliding_forward": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_vp, _c_vp]),
+    "pkv_pruner_create": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_dbl, _c_u32,
+                                         ctypes.POINTER(_c_vp)]),
+    "pkv_pruner_destroy": (None, [_c_vp]),
+    "pkv_pruner_k": (_c_i64, [_c_vp]),
+    "pkv_pruner_run": (ctypes.c_int, [_c_vp] * 10),
+    "pkv_pruner_run_host": (ctypes.c_int, [_c_vp] * 9),
+}
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded libpkv_b200.so with argtypes set. Raises if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    if status == 0:
+        return
+    msg = lib().pkv_last_error().decode(errors="replace")
+    raise _STATUS.get(status, PkvError)(msg)

@@ -1,0 +1,335 @@
+"""Host-side mirror of the reference ProxyKV scoring / mapper / prune API over
+the B200 C ABI (include/pkv_capi.h).
+
+Names, argument meaning and error behaviour follow the reference
+(/root/reference/proj/include/proxykv/{pruning,mapper}.hpp) so the parity tests
+read like the reference's own tests. Device memory is torch-allocated
+(plumbing); every computation runs in libpkv_b200.so's sm_100a kernels.
+There is no CPU fallback: without a B200 every compute call raises
+NoDeviceError.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib
+from ._lib import ConfigError, CudaError, NoDeviceError, PkvError, PkvValueError, ShapeError, check, lib
+
+__all__ = [
+    "Context", "PruneMask", "MaskApplication", "ModelGeometry", "MapperConfig", "Mapper", "Pruner",
+    "retention_count", "topk_select", "topk_mask", "apply_mask", "compact_kv", "score", "score_lse",
+    "layer_pair", "window_offsets", "mapper_init_params", "ShapeError", "PkvValueError", "ConfigError",
+    "CudaError", "NoDeviceError", "PkvError", "SCORE_REDUCE_MAX", "SCORE_REDUCE_SUM", "SCORE_CAUSAL",
+    "MAPPER_FP16", "MAPPER_FP16X2", "MAPPER_FP16X3",
+]
+
+SCORE_REDUCE_MAX = 0
+SCORE_REDUCE_SUM = 1
+SCORE_CAUSAL = 2
+MAPPER_FP16 = 1
+MAPPER_FP16X2 = 2
+MAPPER_FP16X3 = 3
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    torch = _torch()
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+class Context:
+    """pkv_ctx: one per device (and host thread)."""
+
+    _default = {}
+
+    def __init__(self, device: int = 0):
+        h = ctypes.c_void_p()
+        check(lib().pkv_ctx_create(device, ctypes.byref(h)))
+        self.h = h
+        self.device = device
+
+    @classmethod
+    def default(cls, device: int = 0) -> "Context":
+        if device not in cls._default:
+            cls._default[device] = Context(device)
+        return cls._default[device]
+
+    def launches(self) -> int:
+        return int(lib().pkv_ctx_launch_count(self.h))
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h and _lib._lib is not None:
+            _lib._lib.pkv_ctx_destroy(h)
+            self.h = None
+
+
+# ------------------------------------------------------------------ select --
+def retention_count(rho: float, n: int) -> int:
+    """pruning.cpp:14-18."""
+    k = ctypes.c_int64()
+    check(lib().pkv_retention_count(float(rho), int(n), ctypes.byref(k)))
+    return k.value
+
+
+def topk_select(scores, k: int, *, want_mask: bool = True, want_idx: bool = True, ctx: Context = None,
+                stream=None):
+    """Device Top-K: scores fp32 cuda tensor [..., n] -> (mask u8 [..., n] | None, idx i32 [slices, k] | None)."""
+    torch = _torch()
+    ctx = ctx or Context.default(scores.device.index or 0)
+    if scores.dtype != torch.float32 or not scores.is_cuda:
+        raise ShapeError("topk_select expects a float32 CUDA tensor")
+    s = scores.contiguous()
+    n = s.shape[-1]
+    slices = s.numel() // n if n else 0
+    mask = torch.empty(s.shape, dtype=torch.uint8, device=s.device) if want_mask else None
+    idx = torch.empty((slices, max(int(k), 0)), dtype=torch.int32, device=s.device) if want_idx else None
+    check(lib().pkv_topk_select(ctx.h, _ptr(s), slices, n, int(k), _ptr(mask), _ptr(idx), _stream(stream)))
+    return mask, idx
+
+
+@dataclass
+class PruneMask:
+    """pruning.hpp:22-30."""
+    shape: Tuple[int, ...]
+    bits: np.ndarray
+    retention_ratio: float = 1.0
+    k: int = 0
+    idx_asc: Optional[np.ndarray] = None  # [slices, k], from the GPU select
+
+    def token_count(self) -> int:
+        return self.shape[-1]
+
+    def slice_count(self) -> int:
+        return int(np.prod(self.shape)) // self.shape[-1]
+
+
+def topk_mask(scores: np.ndarray, rho: float, ctx: Context = None) -> PruneMask:
+    """pruning.cpp:37-56 with host scores (the reference signature): GPU radix select,
+    mask bits and ascending indices copied back."""
+    torch = _torch()
+    s = np.asarray(scores)
+    if s.ndim == 0:
+        raise ShapeError("topk_mask needs a shaped tensor")
+    n = s.shape[-1]
+    k = retention_count(rho, n)
+    dev = torch.from_numpy(np.ascontiguousarray(s, dtype=np.float32)).cuda()
+    mask, idx = topk_select(dev, k, ctx=ctx)
+    torch.cuda.synchronize()
+    return PruneMask(tuple(s.shape), mask.cpu().numpy(), rho, k, idx.cpu().numpy())
+
+
+@dataclass
+class MaskApplication:
+    """pruning.hpp:48-53."""
+    retained: List[np.ndarray] = field(default_factory=list)
+    dropped_per_slice: int = 0
+    bytes_saved_per_head: int = 0
+    bytes_saved_total: int = 0
+
+
+def apply_mask(mask: PruneMask, head_dim: int, bytes_per_elem: int = 2) -> MaskApplication:
+    """pruning.cpp:197-215: retained indices (ascending, produced on the GPU by the
+    select kernel's ordered compaction) and the byte accounting."""
+    if mask.idx_asc is None:
+        raise PkvValueError("apply_mask needs a PruneMask produced by topk_mask (GPU indices)")
+    n, slices = mask.token_count(), mask.slice_count()
+    app = MaskApplication([mask.idx_asc[s].astype(np.int64) for s in range(slices)])
+    app.dropped_per_slice = n - mask.k
+    app.bytes_saved_per_head = app.dropped_per_slice * head_dim * bytes_per_elem * 2
+    app.bytes_saved_total = app.bytes_saved_per_head * slices
+    return app
+
+
+def compact_kv(k_in, v_in, idx_asc, *, ctx: Context = None, stream=None, out=None):
+    """Packed gather of retained rows: k_in/v_in [S, n, d] (2-byte) cuda, idx_asc i32 [S, k]."""
+    torch = _torch()
+    ctx = ctx or Context.default(k_in.device.index or 0)
+    S, n, d = k_in.shape
+    k = idx_asc.shape[1]
+    if out is None:
+        ko = torch.empty((S, k, d), dtype=k_in.dtype, device=k_in.device)
+        vo = torch.empty((S, k, d), dtype=v_in.dtype, device=v_in.device)
+    else:
+        ko, vo = out
+    check(lib().pkv_compact_kv(ctx.h, _ptr(k_in), _ptr(v_in), _ptr(idx_asc), S, n, k, d, k_in.element_size(),
+                               _ptr(ko), _ptr(vo), _stream(stream)))
+    return ko, vo
+
+
+# ----------------------------------------------------------------- scoring --
+def score(q, k, *, reduce: str = "max", causal: bool = False, lse=None, ctx: Context = None, stream=None, out=None):
+    """Proxy scoring: q bf16 [L, Hq, Nq, d], k bf16 [L, Hkv, Nk, d] -> X fp32 [L, Hkv, Nk]."""
+    torch = _torch()
+    ctx = ctx or Context.default(q.device.index or 0)
+    L, hq, nq, d = q.shape
+    _, hkv, nk, _ = k.shape
+    flags = (SCORE_REDUCE_SUM if reduce == "sum" else SCORE_REDUCE_MAX) | (SCORE_CAUSAL if causal else 0)
+    x = out if out is not None else torch.empty((L, hkv, nk), dtype=torch.float32, device=q.device)
+    check(lib().pkv_score(ctx.h, _ptr(q), _ptr(k), L, hq, hkv, nq, nk, d, flags, _ptr(lse), _ptr(x),
+                          _stream(stream)))
+    return x
+
+
+def score_lse(q, k, *, causal: bool = False, ctx: Context = None, stream=None):
+    torch = _torch()
+    ctx = ctx or Context.default(q.device.index or 0)
+    L, hq, nq, d = q.shape
+    _, hkv, nk, _ = k.shape
+    out = torch.empty((L, hq, nq), dtype=torch.float32, device=q.device)
+    check(lib().pkv_score_lse(ctx.h, _ptr(q), _ptr(k), L, hq, hkv, nq, nk, d, SCORE_CAUSAL if causal else 0,
+                              _ptr(out), _stream(stream)))
+    return out
+
+
+# ------------------------------------------------------------------ mapper --
+@dataclass
+class ModelGeometry:
+    """mapper.hpp:16-25."""
+    target_layers: int = 32
+    target_heads: int = 32
+    proxy_layers: int = 16
+    proxy_heads: int = 32
+    head_dim: int = 128
+
+    def as5(self):
+        return (ctypes.c_int64 * 5)(self.target_layers, self.target_heads, self.proxy_layers, self.proxy_heads,
+                                    self.head_dim)
+
+
+@dataclass
+class MapperConfig:
+    """mapper.hpp:35-55 (stage modes 'active' | 'bypass')."""
+    d_time: int = 512
+    encoder_layers: int = 6
+    encoder_heads: int = 8
+    ffn_mult: int = 4
+    d_head: int = 64
+    crop_len: int = 2048
+    stride: int = 1024
+    synthetic_heads: int = 0
+    stage_conv: str = "active"
+    stage_encoder: str = "active"
+    stage_cross: str = "active"
+    normalize_input: bool = False
+
+    def as12(self):
+        m = {"active": 0, "bypass": 1}
+        for s in (self.stage_conv, self.stage_encoder, self.stage_cross):
+            if s not in m:
+                raise ConfigError(f"unknown stage mode '{s}' (expected active|bypass)")
+        return (ctypes.c_int64 * 12)(self.d_time, self.encoder_layers, self.encoder_heads, self.ffn_mult,
+                                     self.d_head, self.crop_len, self.stride, self.synthetic_heads,
+                                     m[self.stage_conv], m[self.stage_encoder], m[self.stage_cross],
+                                     int(self.normalize_input))
+
+
+def layer_pair(target_layer: int, geom: ModelGeometry) -> int:
+    """mapper.cpp:44-49."""
+    out = ctypes.c_int64()
+    check(lib().pkv_layer_pair(int(target_layer), geom.as5(), ctypes.byref(out)))
+    return out.value
+
+
+def window_offsets(n: int, crop: int, stride: int) -> List[int]:
+    """mapper.cpp:66-79."""
+    cnt = ctypes.c_int64()
+    check(lib().pkv_window_offsets(n, crop, stride, None, 0, ctypes.byref(cnt)))
+    buf = (ctypes.c_int64 * max(cnt.value, 1))()
+    check(lib().pkv_window_offsets(n, crop, stride, buf, cnt.value, ctypes.byref(cnt)))
+    return list(buf[:cnt.value])
+
+
+def mapper_init_params(geom: ModelGeometry, cfg: MapperConfig, seed: int) -> np.ndarray:
+    """MapperParams::init (mapper.cpp:97-164) as the flat fp64 parameter blob."""
+    cnt = ctypes.c_int64()
+    check(lib().pkv_mapper_init_params(geom.as5(), cfg.as12(), seed, None, ctypes.byref(cnt)))
+    blob = np.zeros(cnt.value, np.float64)
+    check(lib().pkv_mapper_init_params(geom.as5(), cfg.as12(), seed, blob.ctypes.data, ctypes.byref(cnt)))
+    return blob
+
+
+class Mapper:
+    """Device-resident HybridAxialMapper (pkv_mapper)."""
+
+    def __init__(self, geom: ModelGeometry, cfg: MapperConfig, blob: np.ndarray = None, *, seed: int = 0,
+                 precision: int = MAPPER_FP16X2, ctx: Context = None):
+        self.geom, self.cfg = geom, cfg
+        self.ctx = ctx or Context.default()
+        if blob is None:
+            blob = mapper_init_params(geom, cfg, seed)
+        blob = np.ascontiguousarray(blob, np.float64)
+        h = ctypes.c_void_p()
+        check(lib().pkv_mapper_create(self.ctx.h, geom.as5(), cfg.as12(), blob.ctypes.data, blob.size,
+                                      precision, ctypes.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h and _lib._lib is not None:
+            _lib._lib.pkv_mapper_destroy(h)
+            self.h = None
+
+    def forward_full(self, x_all, stream=None, out=None):
+        """x_all fp32 cuda [B, L_s, H_s, N] -> [B, L_l, H_l, N]."""
+        torch = _torch()
+        B, ls, hs, n = x_all.shape
+        x = x_all.contiguous()
+        y = out if out is not None else torch.empty((B, self.geom.target_layers, self.geom.target_heads, n),
+                                                    dtype=torch.float32, device=x.device)
+        check(lib().pkv_mapper_forward_full(self.h, _ptr(x), B, n, _ptr(y), _stream(stream)))
+        return y
+
+    def sliding_forward(self, x, stream=None):
+        """x fp32 cuda [B, H_s, N] -> [B, H_l, N] (forward_pair when N <= crop_len)."""
+        torch = _torch()
+        B, hs, n = x.shape
+        x = x.contiguous()
+        y = torch.empty((B, self.geom.target_heads, n), dtype=torch.float32, device=x.device)
+        check(lib().pkv_mapper_sliding_forward(self.h, _ptr(x), B, n, _ptr(y), _stream(stream)))
+        return y
+
+    forward_pair = sliding_forward
+
+
+class Pruner:
+    """pkv_pruner: score -> map -> select -> compact for one context shape."""
+
+    def __init__(self, mapper: Mapper, Hq: int, dp: int, dt: int, N: int, rho: float, *, reduce: str = "max",
+                 causal: bool = False):
+        self.mapper = mapper
+        flags = (SCORE_REDUCE_SUM if reduce == "sum" else SCORE_REDUCE_MAX) | (SCORE_CAUSAL if causal else 0)
+        h = ctypes.c_void_p()
+        check(lib().pkv_pruner_create(mapper.ctx.h, mapper.h, Hq, dp, dt, N, float(rho), flags, ctypes.byref(h)))
+        self.h = h
+        self.k = int(lib().pkv_pruner_k(h))
+        self.N = N
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h and _lib._lib is not None:
+            _lib._lib.pkv_pruner_destroy(h)
+            self.h = None
+
+    def run(self, q, kp, kt, vt, k_out, v_out, idx_out=None, scores_out=None, stream=None):
+        check(lib().pkv_pruner_run(self.h, _ptr(q), _ptr(kp), _ptr(kt), _ptr(vt), _ptr(k_out), _ptr(v_out),
+                                   _ptr(idx_out), _ptr(scores_out), _stream(stream)))
+
+    def run_host(self, q, kp, kt, vt, k_out, v_out, idx_out=None, stream=None):
+        """Host (ideally pinned) torch tensors in and out; copies happen inside the call."""
+        check(lib().pkv_pruner_run_host(self.h, _ptr(q), _ptr(kp), _ptr(kt), _ptr(vt), _ptr(k_out), _ptr(v_out),
+                                        _ptr(idx_out), _stream(stream)))

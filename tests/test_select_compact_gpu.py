@@ -1,0 +1,124 @@
+"""GPU parity of Top-K select (+ ascending index lists) and KV compaction,
+through the C ABI, against the reference's golden vectors and the oracle.
+Bit-exact bar (integer / index / byte work)."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import pkv_oracle as O
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pr():
+    return np.load(os.path.join(GOLD, "pruning.npz"))
+
+
+def _sel(scores_np, k, ctx):
+    import torch
+    import paper_2605_16360_b200 as P
+    dev = torch.from_numpy(np.ascontiguousarray(scores_np, np.float32)).cuda()
+    mask, idx = P.topk_select(dev, k, ctx=ctx)
+    torch.cuda.synchronize()
+    return mask.cpu().numpy(), idx.cpu().numpy()
+
+
+def test_basic_and_errors(gpu, pr):
+    import paper_2605_16360_b200 as P
+    for name, want in [("basic", [0, 2]), ("basic_all", [0, 1, 2]), ("tie", [0]), ("loss_gt", [0, 2])]:
+        m = P.topk_mask(pr[f"{name}_scores"].reshape(1, 1, -1), float(pr[f"{name}_rho"]))
+        assert m.k == int(pr[f"{name}_k"])
+        assert np.flatnonzero(m.bits).tolist() == want
+        assert P.apply_mask(m, 128).retained[0].tolist() == want
+    y = np.array([[[3.0, 1.0, 2.0]]])
+    with pytest.raises(P.PkvValueError):
+        P.topk_mask(y, 0.0)
+    with pytest.raises(P.PkvValueError):
+        P.topk_mask(y, 1.5)
+
+
+def test_exhaustive_3pow8(gpu, pr):
+    vecs = pr["exhaustive_vectors"]
+    for k in range(1, 9):
+        mask, idx = _sel(vecs, k, gpu)
+        np.testing.assert_array_equal(mask, pr["exhaustive_bits"][k - 1])
+        for r in (0, 100, 6560):
+            assert idx[r].tolist() == np.flatnonzero(mask[r]).tolist()
+
+
+def test_tie_heavy_1000(gpu, pr):
+    for v, k, bits in zip(pr["ties_vectors"], pr["ties_k"], pr["ties_bits"]):
+        mask, idx = _sel(v[None], int(k), gpu)
+        np.testing.assert_array_equal(mask[0], bits)
+        assert idx[0].tolist() == np.flatnonzero(bits).tolist()
+
+
+def test_affine_invariance(gpu, pr):
+    for v, a, c, bits in zip(pr["affine_vectors"], pr["affine_alpha"], pr["affine_c"], pr["affine_bits"]):
+        k = O.retention_count(0.25, 16)
+        m1, _ = _sel(v, k, gpu)
+        m2, _ = _sel((a * v + c), k, gpu)
+        np.testing.assert_array_equal(m1, bits)
+        np.testing.assert_array_equal(m2, bits)
+
+
+def test_apply_mask_bytes(gpu, pr):
+    import paper_2605_16360_b200 as P
+    m = P.topk_mask(pr["apply_big_scores"], 0.5)
+    app = P.apply_mask(m, 128, 2)
+    np.testing.assert_array_equal(app.retained[0], pr["apply_big_idx"][0])
+    assert app.bytes_saved_per_head == 262144
+    assert P.apply_mask(P.topk_mask(pr["apply_big_scores"], 1.0), 128, 2).bytes_saved_per_head == 0
+
+
+def test_signed_zero_subnormal_allequal(gpu, pr):
+    mask, idx = _sel(pr["rand_scores"], int(pr["rand_k"]), gpu)
+    np.testing.assert_array_equal(mask, pr["rand_bits"])
+    np.testing.assert_array_equal(idx.reshape(pr["rand_idx"].shape), pr["rand_idx"])
+
+
+@pytest.mark.parametrize("slices,n,rho", [(256, 32768, 0.2), (112, 131072, 0.2), (4, 170000, 0.07), (3, 1, 1.0),
+                                          (5, 4099, 0.5), (7, 12, 0.1), (2, 65536, 0.5)])
+def test_vs_oracle_shapes(gpu, slices, n, rho):
+    r = np.random.RandomState(n % 1000 + slices)
+    s = r.uniform(0, 1, (slices, n)).astype(np.float32)
+    if n > 8:
+        s[0, : n // 3] = np.round(s[0, : n // 3] * 64) / 64  # ties
+    k = O.retention_count(rho, n)
+    mask, idx = _sel(s, k, gpu)
+    omask, oidx = O.topk_select(s, k)
+    np.testing.assert_array_equal(mask, omask)
+    np.testing.assert_array_equal(idx, oidx)
+
+
+def test_index_only_output(gpu):
+    import torch
+    import paper_2605_16360_b200 as P
+    s = torch.rand(8, 5000, device="cuda")
+    k = 1000
+    _, idx = P.topk_select(s, k, want_mask=False, ctx=gpu)
+    _, oidx = O.topk_select(s.cpu().numpy(), k)
+    np.testing.assert_array_equal(idx.cpu().numpy(), oidx)
+
+
+@pytest.mark.parametrize("S,n,k,d,dtype", [(256, 32768, 6554, 128, "bf16"), (8, 1000, 333, 64, "fp16"),
+                                           (3, 50, 11, 4, "bf16"), (2, 77, 5, 3, "bf16")])
+def test_compaction_bit_exact(gpu, S, n, k, d, dtype):
+    import torch
+    import paper_2605_16360_b200 as P
+    g = torch.Generator(device="cuda").manual_seed(5)
+    kin = torch.randint(0, 1 << 15, (S, n, d), device="cuda", dtype=torch.int32, generator=g).to(torch.int16)
+    vin = torch.randint(0, 1 << 15, (S, n, d), device="cuda", dtype=torch.int32, generator=g).to(torch.int16)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float16
+    kin, vin = kin.view(tdt), vin.view(tdt)
+    scores = torch.rand(S, n, device="cuda", generator=g)
+    _, idx = P.topk_select(scores, k, want_mask=False, ctx=gpu)
+    ko, vo = P.compact_kv(kin, vin, idx, ctx=gpu)
+    torch.cuda.synchronize()
+    kb, vb = kin.view(torch.int16).cpu().numpy().view(np.uint16), vin.view(torch.int16).cpu().numpy().view(np.uint16)
+    eko, evo = O.compact_kv(kb, vb, idx.cpu().numpy())
+    np.testing.assert_array_equal(ko.view(torch.int16).cpu().numpy().view(np.uint16), eko)
+    np.testing.assert_array_equal(vo.view(torch.int16).cpu().numpy().view(np.uint16), evo)
