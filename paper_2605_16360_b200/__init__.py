@@ -2,5 +2,5 @@
 HybridAxialMapper -> Top-K select -> KV compaction, behind the reference's
 scoring / mapper / prune API (see include/pkv_capi.h)."""
 from . import proxykv  # noqa: F401
-from ._lib import LIB_PATH, lib  # noqa: F401
+from ._lib import LIB_PATH, check, lib  # noqa: F401
 from .proxykv import *  # noqa: F401,F403

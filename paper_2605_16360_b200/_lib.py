@@ -89,7 +89,10 @@ def lib() -> ctypes.CDLL:
             raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
         L = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
-            fn = getattr(L, name)
+            try:
+                fn = getattr(L, name)
+            except AttributeError:  # reported by tests/test_capi.py::test_every_header_symbol_exported
+                continue
             fn.restype = res
             fn.argtypes = args
         _lib = L

@@ -1,0 +1,304 @@
+// gemm.cu — see gemm.cuh. Persistent, warp-specialised tcgen05 GEMM.
+//   warp 0 : TMA producer (one elected lane)
+//   warp 1 : MMA issuer (one elected lane)
+//   warp 2 : TMEM allocator
+//   warps 4-7 : epilogue (thread = accumulator row; TMEM lane quadrant = warp % 4)
+#include "gemm.cuh"
+
+namespace pkv {
+namespace {
+
+using namespace sm100;
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;  // one 128-B swizzle atom of fp16
+constexpr int kThreads = 256;
+constexpr int kABytes = kBM * kBK * 2;
+
+__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+
+template <int BN, int NA, int NB>
+struct Cfg {
+    static constexpr int kBBytes = BN * kBK * 2;
+    static constexpr int kStageBytes = NA * kABytes + NB * kBBytes;
+    static constexpr int kBudget = 227 * 1024 - 2048;
+    static constexpr int kStagesRaw = kBudget / kStageBytes;
+    static constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
+    static constexpr int kSmem = 1024 + kStages * kStageBytes + 256;
+    static constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+    static_assert(kStages >= 2, "not enough shared memory for 2 stages");
+};
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const GemmEpiParams& p, int64_t row, int64_t col0, int64_t N,
+                                               const uint32_t (&r)[32]) {
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+    const bool full = (col0 + 32 <= N);
+    if (p.bias) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] += (full || col0 + j < N) ? __ldg(p.bias + col0 + j) : 0.0f;
+    }
+    if (EPI == EPI_GELU_F16X || EPI == EPI_GELU_PE) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+    }
+    const int64_t base = row * p.ldo + col0;
+    if (EPI == EPI_F16X || EPI == EPI_GELU_F16X) {
+        if (full) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+                __align__(16) __half hi[8];
+                __align__(16) __half lo[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    hi[t] = __float2half_rn(v[j + t]);
+                    lo[t] = __float2half_rn(v[j + t] - __half2float(hi[t]));
+                }
+                *reinterpret_cast<uint4*>(p.out_h + base + j) = *reinterpret_cast<const uint4*>(hi);
+                if (p.out_l) *reinterpret_cast<uint4*>(p.out_l + base + j) = *reinterpret_cast<const uint4*>(lo);
+            }
+        } else {
+            for (int j = 0; j < 32 && col0 + j < N; ++j) {
+                const __half hi = __float2half_rn(v[j]);
+                p.out_h[base + j] = hi;
+                if (p.out_l) p.out_l[base + j] = __float2half_rn(v[j] - __half2float(hi));
+            }
+        }
+        return;
+    }
+    if (EPI == EPI_GELU_PE) {
+        const float* pe = p.pe + (row % p.lw) * p.ldo + col0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] += (full || col0 + j < N) ? __ldg(pe + j) : 0.0f;
+    }
+    float* out = p.out_f32 + base;
+    if (EPI == EPI_RESID) {
+        if (full) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+                float4 o = *reinterpret_cast<float4*>(out + j);
+                o.x += v[j];
+                o.y += v[j + 1];
+                o.z += v[j + 2];
+                o.w += v[j + 3];
+                *reinterpret_cast<float4*>(out + j) = o;
+            }
+        } else {
+            for (int j = 0; j < 32 && col0 + j < N; ++j) out[j] += v[j];
+        }
+        return;
+    }
+    if (full) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(out + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    } else {
+        for (int j = 0; j < 32 && col0 + j < N; ++j) out[j] = v[j];
+    }
+}
+
+template <int BN, int NA, int NB, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tA0, const __grid_constant__ CUtensorMap tA1,
+                const __grid_constant__ CUtensorMap tB0, const __grid_constant__ CUtensorMap tB1, GemmEpiParams p,
+                int64_t M, int64_t N, int64_t K) {
+    using C = Cfg<BN, NA, NB>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+    uint64_t* empty = full + C::kStages;
+    uint64_t* tfull = empty + C::kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    const int64_t tiles_m = (M + kBM - 1) / kBM, tiles_n = (N + BN - 1) / BN;
+    const int64_t tiles = tiles_m * tiles_n;
+    const int num_kb = (int)((K + kBK - 1) / kBK);
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tA0);
+        tma_prefetch(&tB0);
+        if (NA > 1) tma_prefetch(&tA1);
+        if (NB > 1) tma_prefetch(&tB1);
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int32_t m0 = (int32_t)((t / tiles_n) * kBM);
+                const int32_t n0 = (int32_t)((t % tiles_n) * BN);
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* st = smem + stage * C::kStageBytes;
+                    mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                    tma_load_2d(st, &tA0, &full[stage], kb * kBK, m0);
+                    if (NA > 1) tma_load_2d(st + kABytes, &tA1, &full[stage], kb * kBK, m0);
+                    tma_load_2d(st + NA * kABytes, &tB0, &full[stage], kb * kBK, n0);
+                    if (NB > 1) tma_load_2d(st + NA * kABytes + C::kBBytes, &tB1, &full[stage], kb * kBK, n0);
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc = idesc_f16(kBM, BN, 0);
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+            mbar_wait(&tempty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t d = tmem_base + acc * BN;
+            for (int kb = 0; kb < num_kb; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                if (elect_one()) {
+                    uint8_t* st = smem + stage * C::kStageBytes;
+                    const uint64_t a0 = desc_sw128(st);
+                    const uint64_t a1 = desc_sw128(st + kABytes);
+                    const uint64_t b0 = desc_sw128(st + NA * kABytes);
+                    const uint64_t b1 = desc_sw128(st + NA * kABytes + C::kBBytes);
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        const uint64_t off = (uint64_t)(kk * 2);  // +32 B within the swizzle atom
+                        mma_f16_ss(d, a0 + off, b0 + off, idesc, (kb | kk) != 0);
+                        if (NA > 1) mma_f16_ss(d, a1 + off, b0 + off, idesc, 1);
+                        if (NB > 1) mma_f16_ss(d, a0 + off, b1 + off, idesc, 1);
+                    }
+                    mma_commit(&empty[stage]);
+                }
+                __syncwarp();
+                if (++stage == C::kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (elect_one()) mma_commit(&tfull[acc]);
+            __syncwarp();
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    } else if (warp >= 4) {
+        const uint32_t quad = warp & 3;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+            const int64_t m0 = (t / tiles_n) * kBM;
+            const int64_t n0 = (t % tiles_n) * BN;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int64_t row = m0 + quad * 32 + lane;
+            const uint32_t taddr = tmem_base + ((quad * 32) << 16) + acc * BN;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t r[32];
+                tmem_ld32(taddr + c0, r);
+                tmem_ld_wait();
+                if (row < M && n0 + c0 < N) epilogue_chunk<EPI>(p, row, n0 + c0, N, r);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, C::kTmemCols);
+    }
+}
+
+template <int BN, int NA, int NB, int EPI>
+void launch(const GemmArgs& g, int sm_count, cudaStream_t st) {
+    using C = Cfg<BN, NA, NB>;
+    auto kern = gemm_kernel<BN, NA, NB, EPI>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        PKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+        attr_set = true;
+    }
+    const int64_t tiles = ((g.M + kBM - 1) / kBM) * ((g.N + BN - 1) / BN);
+    const int grid = (int)(tiles < sm_count ? tiles : sm_count);
+    kern<<<grid, kThreads, C::kSmem, st>>>(g.a[0], g.a[1], g.b[0], g.b[1], g.p, g.M, g.N, g.K);
+    check_launch("gemm_kernel");
+}
+
+template <int BN, int NA, int NB>
+void dispatch_epi(const GemmArgs& g, int sm, cudaStream_t st) {
+    switch (g.epi) {
+        case EPI_F32: return launch<BN, NA, NB, EPI_F32>(g, sm, st);
+        case EPI_F16X: return launch<BN, NA, NB, EPI_F16X>(g, sm, st);
+        case EPI_GELU_F16X: return launch<BN, NA, NB, EPI_GELU_F16X>(g, sm, st);
+        case EPI_RESID: return launch<BN, NA, NB, EPI_RESID>(g, sm, st);
+        case EPI_GELU_PE: return launch<BN, NA, NB, EPI_GELU_PE>(g, sm, st);
+    }
+}
+
+template <int BN>
+void dispatch_planes(const GemmArgs& g, int sm, cudaStream_t st) {
+    if (g.na == 1 && g.nb == 1) return dispatch_epi<BN, 1, 1>(g, sm, st);
+    if (g.na == 2 && g.nb == 1) return dispatch_epi<BN, 2, 1>(g, sm, st);
+    if (g.na == 2 && g.nb == 2) return dispatch_epi<BN, 2, 2>(g, sm, st);
+    throw Error{PKV_ECONFIG, cat("unsupported GEMM plane combination na=", g.na, " nb=", g.nb)};
+}
+
+}  // namespace
+
+void gemm_set_a(GemmArgs& g, int plane, const __half* a, int64_t M, int64_t K, int64_t lda) {
+    g.a[plane] = make_tmap_2d(a, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, (uint64_t)K, (uint64_t)M, (uint64_t)lda * 2, kBK, kBM,
+                              CU_TENSOR_MAP_SWIZZLE_128B);
+    if (plane == 0 && g.na < 1) g.na = 1;
+    if (plane == 1) g.na = 2;
+    g.M = M;
+    g.K = K;
+}
+
+void gemm_set_b(GemmArgs& g, int plane, const __half* b, int64_t N, int64_t K, int64_t ldb) {
+    g.b[plane] = make_tmap_2d(b, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, (uint64_t)K, (uint64_t)N, (uint64_t)ldb * 2, kBK,
+                              (uint32_t)g.bn, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (plane == 1) g.nb = 2;
+    g.N = N;
+}
+
+void gemm_run(const GemmArgs& g, int sm_count, cudaStream_t st) {
+    if (g.M == 0 || g.N == 0) return;
+    if (g.na == 1) {
+        // the plane-1 map is never dereferenced; pass plane 0 to keep the params valid
+    }
+    switch (g.bn) {
+        case 256: return dispatch_planes<256>(g, sm_count, st);
+        case 128: return dispatch_planes<128>(g, sm_count, st);
+        case 64: return dispatch_planes<64>(g, sm_count, st);
+        default: throw Error{PKV_ECONFIG, cat("unsupported GEMM tile N ", g.bn)};
+    }
+}
+
+}  // namespace pkv
