@@ -22,6 +22,11 @@ pkv_status pkv_test_gemm(pkv_ctx ctx, const float* a_dev, int64_t M, int64_t K, 
                          int na, int nb, int bn, int epi, const float* bias_dev, const float* pe_dev, int64_t lw,
                          float* out_dev, void* stream);
 
+/* Encoder self-attention (mapper.cpp:254-270) on fp32 qkv [nwin*Lw, 3*D]
+ * rounded to fp16: out fp32 [nwin*Lw, D] (recombined hi+lo planes). */
+pkv_status pkv_test_attention(pkv_ctx ctx, const float* qkv_dev, int64_t nwin, int64_t Lw, int64_t D, int64_t heads,
+                              float* out_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

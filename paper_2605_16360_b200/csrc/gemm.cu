@@ -68,7 +68,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpiParams& p, int64_t r
         }
         return;
     }
-    if (EPI == EPI_GELU_PE) {
+    if (EPI == EPI_GELU_PE && p.pe) {
         const float* pe = p.pe + (row % p.lw) * p.ldo + col0;
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] += (full || col0 + j < N) ? __ldg(pe + j) : 0.0f;

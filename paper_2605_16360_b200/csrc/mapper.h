@@ -1,0 +1,81 @@
+// mapper.h — host-side HybridAxialMapper state (see mapper.cpp).
+#pragma once
+#include <cuda_fp16.h>
+
+#include <memory>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "gemm.cuh"
+#include "internal.h"
+
+namespace pkv {
+
+// ModelGeometry, proj/include/proxykv/mapper.hpp:16-25
+struct Geometry {
+    int64_t target_layers = 32, target_heads = 32, proxy_layers = 16, proxy_heads = 32, head_dim = 128;
+    static Geometry from5(const int64_t* g);
+    void validate() const;
+};
+
+// MapperConfig, proj/include/proxykv/mapper.hpp:35-55
+struct Config {
+    int64_t d_time = 512, encoder_layers = 6, encoder_heads = 8, ffn_mult = 4, d_head = 64, crop_len = 2048,
+            stride = 1024, synthetic_heads = 0;
+    bool conv_active = true, enc_active = true, cross_active = true, normalize_input = false;
+    static Config from12(const int64_t* c);
+    void validate() const;
+    int64_t conv_mid() const { return d_time / 2 > 0 ? d_time / 2 : 1; }
+    int64_t syn(const Geometry& g) const { return synthetic_heads > 0 ? synthetic_heads : g.proxy_heads; }
+};
+
+int64_t layer_pair(int64_t ll, const Geometry& g);
+std::vector<int64_t> window_offsets(int64_t n, int64_t crop, int64_t stride);
+std::vector<std::pair<std::string, int64_t>> param_layout(const Geometry& g, const Config& c);
+std::vector<double> init_params(const Geometry& g, const Config& c, uint64_t seed);
+
+struct WeightPlanes {
+    __half* hi = nullptr;
+    __half* lo = nullptr;
+    int64_t N = 0, K = 0;  // B operand [N, K], K-major
+};
+
+struct Block {
+    WeightPlanes qkv, o, f1, f2;
+    float *qkv_b = nullptr, *o_b = nullptr, *f1_b = nullptr, *f2_b = nullptr;
+    float *ln1_g = nullptr, *ln1_b = nullptr, *ln2_g = nullptr, *ln2_b = nullptr;
+};
+
+class Mapper {
+public:
+    Mapper(pkv_ctx ctx, const Geometry& g, const Config& c, const double* blob, int64_t count, uint32_t precision);
+    ~Mapper();
+    void run(const float* x, const std::vector<int64_t>& unit_off, int64_t N, const std::vector<int>& out_unit,
+             float* y, cudaStream_t st);
+
+    pkv_ctx ctx;
+    Geometry geom;
+    Config cfg;
+    int na = 2, nb = 1;
+    int64_t rows_cap = int64_t(1) << 20;  // rows per chunk (bounds the workspace)
+
+private:
+    WeightPlanes upload_planes(const std::vector<double>& W, int64_t N, int64_t K);
+    void gemm(const __half* a_h, const __half* a_l, int64_t M, const WeightPlanes& w, const float* bias, GemmEpi epi,
+              GemmEpiParams p, cudaStream_t st);
+
+    std::vector<void*> owned;
+    DevBuf work;
+    float* pe_d = nullptr;
+    float *conv1_w = nullptr, *conv1_b = nullptr, *conv2_b = nullptr;
+    WeightPlanes conv2;
+    float *bypass_w = nullptr, *bypass_b = nullptr;
+    std::vector<Block> blocks;
+    WeightPlanes stage3;
+    float* stage3_b = nullptr;
+    float out_b = 0.0f;
+    int64_t n3 = 0, ld3 = 0;
+};
+
+}  // namespace pkv

@@ -1,6 +1,7 @@
 // test_hooks.cpp — unit-test entry points (include/pkv_test_hooks.h).
 #include "../../include/pkv_test_hooks.h"
 
+#include "attn.cuh"
 #include "gemm.cuh"
 #include "util.cuh"
 
@@ -41,6 +42,23 @@ extern "C" pkv_status pkv_test_gemm(pkv_ctx ctx, const float* a_dev, int64_t M, 
         }
         gemm_run(g, ctx->sm_count, st);
         if (planes) launch_combine_f16(oh, ol, (int64_t)o_el, out_dev, st);
+        PKV_CUDA(cudaStreamSynchronize(st));
+        count_launch(ctx, 3);
+    });
+}
+
+extern "C" pkv_status pkv_test_attention(pkv_ctx ctx, const float* qkv_dev, int64_t nwin, int64_t Lw, int64_t D,
+                                         int64_t heads, float* out_dev, void* stream) {
+    return guard([&] {
+        require_ctx(ctx);
+        auto st = static_cast<cudaStream_t>(stream);
+        DevBuf buf;
+        const size_t in_el = (size_t)(nwin * Lw * 3 * D), o_el = (size_t)(nwin * Lw * D);
+        auto* base = static_cast<__half*>(buf.get((in_el + 2 * o_el) * sizeof(__half)));
+        __half *q = base, *oh = q + in_el, *ol = oh + o_el;
+        launch_split_f16(qkv_dev, (int64_t)in_el, q, nullptr, st);
+        launch_encoder_attention(q, nwin, Lw, D, heads, oh, ol, D, st);
+        launch_combine_f16(oh, ol, (int64_t)o_el, out_dev, st);
         PKV_CUDA(cudaStreamSynchronize(st));
         count_launch(ctx, 3);
     });

@@ -84,3 +84,23 @@ def test_gemm_fused_epilogues(gpu, epi):
         want = gelu(x) + pe.double()[rows]
     err = (out.double() - want).abs().max().item()
     assert err <= 1e-5 * max(1.0, want.abs().max().item()), err
+
+
+@pytest.mark.parametrize("nwin,Lw,heads", [(1, 128, 1), (2, 256, 8), (3, 200, 8), (2, 2048, 8), (1, 77, 2)])
+def test_encoder_attention(gpu, nwin, Lw, heads):
+    import torch
+    import paper_2605_16360_b200 as P
+    D = 64 * heads
+    f = P.lib().pkv_test_attention
+    f.restype = ctypes.c_int
+    f.argtypes = [ctypes.c_void_p, ctypes.c_void_p] + [ctypes.c_int64] * 4 + [ctypes.c_void_p, ctypes.c_void_p]
+    g = torch.Generator(device="cuda").manual_seed(Lw)
+    qkv = torch.randn(nwin * Lw, 3 * D, device="cuda", generator=g) * 1.5
+    out = torch.full((nwin * Lw, D), float("nan"), device="cuda")
+    P.check(f(gpu.h, qkv.data_ptr(), nwin, Lw, D, heads, out.data_ptr(), None))
+    x = _f16_round(qkv).view(nwin, Lw, 3, heads, 64)
+    q, k, v = (x[:, :, i].permute(0, 2, 1, 3) for i in range(3))  # [nwin, heads, Lw, 64]
+    a = torch.softmax((q @ k.transpose(-1, -2)) / 8.0, dim=-1)
+    want = (a @ v).permute(0, 2, 1, 3).reshape(nwin * Lw, D)
+    err = (out.double() - want).abs().max().item()
+    assert err < 3e-3 * want.abs().max().item(), err
