@@ -193,3 +193,40 @@ pkv_status pkv_compact_kv(pkv_ctx ctx, const void* k_in_dev, const void* v_in_de
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------- scoring ----
+#include "score.cuh"
+
+extern "C" {
+
+pkv_status pkv_score(pkv_ctx ctx, const void* q_dev, const void* k_dev, int64_t L, int64_t Hq, int64_t Hkv,
+                     int64_t Nq, int64_t Nk, int64_t d, uint32_t flags, const float* lse_dev, float* x_out_dev,
+                     void* stream) {
+    return pkv::guard([&] {
+        pkv::require_ctx(ctx);
+        pkv::ScoreShape s{L, Hq, Hkv, Nq, Nk, d, (flags & PKV_SCORE_CAUSAL) != 0};
+        pkv::score_validate(s);
+        auto st = static_cast<cudaStream_t>(stream);
+        auto* lam = static_cast<__nv_bfloat16*>(ctx->scratch_score.get((size_t)(L * Hq * Nq) * 16));
+        if (lse_dev) {
+            pkv::launch_lam_from_lse(lse_dev, L * Hq * Nq, d, lam, st);
+        } else {
+            pkv::launch_score_lse(s, q_dev, k_dev, nullptr, lam, st);
+        }
+        pkv::launch_score_pool(s, q_dev, k_dev, lam, (flags & PKV_SCORE_REDUCE_SUM) == 0, x_out_dev, st);
+        pkv::count_launch(ctx, 2);
+    });
+}
+
+pkv_status pkv_score_lse(pkv_ctx ctx, const void* q_dev, const void* k_dev, int64_t L, int64_t Hq, int64_t Hkv,
+                         int64_t Nq, int64_t Nk, int64_t d, uint32_t flags, float* lse_out_dev, void* stream) {
+    return pkv::guard([&] {
+        pkv::require_ctx(ctx);
+        pkv::ScoreShape s{L, Hq, Hkv, Nq, Nk, d, (flags & PKV_SCORE_CAUSAL) != 0};
+        pkv::score_validate(s);
+        pkv::launch_score_lse(s, q_dev, k_dev, lse_out_dev, nullptr, static_cast<cudaStream_t>(stream));
+        pkv::count_launch(ctx);
+    });
+}
+
+}  // extern "C"

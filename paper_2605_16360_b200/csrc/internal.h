@@ -76,6 +76,7 @@ struct pkv_ctx_s {
     std::atomic<int64_t> launches{0};
     pkv::DevBuf scratch_select;
     pkv::DevBuf scratch_host_io;
+    pkv::DevBuf scratch_score;
 };
 
 namespace pkv {

@@ -1,0 +1,483 @@
+// score.cu — proxy reconstruction-importance scoring (SPEC.md:423-431
+// accumulate_attention; X definition; north-star max-pool), flash
+// style on tcgen05 so the N_q×N_k attention matrix is never materialised:
+//
+//   pass 1 (score_lse_kernel):  S = Q·Kᵀ (M = 128 queries, N = 256 keys) into
+//     TMEM; one thread per query row keeps an online (max, Σexp2) in registers;
+//     writes lse[q] and the bf16 triple (hi, mid, lo) of λ_q = √d·lse_q.
+//   pass 2 (score_pool_kernel): Sᵀ' = K·Qᵀ − λ (M = 128 keys, N = 256 queries),
+//     the −λ_q column folded into the MMA as 3 extra K columns (K_aug = 1,
+//     Q_aug = −(hi, mid, lo)); one thread per key row reduces over queries in
+//     registers: max mode = one FMNMX per element (max_q P = exp2(c·max_q S'),
+//     c = log2(e)/√d); sum mode = exp2 + FADD per element.
+// GQA: pass 2 walks the queries of all heads of a KV head's group.
+//
+// q bf16 [L, Hq, Nq, d], k bf16 [L, Hkv, Nk, d]; d ∈ {64, 128}.
+#include "score.cuh"
+#include "sm100.cuh"
+
+namespace pkv {
+namespace {
+
+using namespace sm100;
+
+constexpr int kThreads = 256;
+constexpr float kLog2e = 1.4426950408889634f;
+
+template <int D>
+struct P1 {
+    static constexpr int kBQ = 128, kBK = 256;
+    static constexpr int kPanels = D / 64;
+    static constexpr int kQBytes = kBQ * D * 2;
+    static constexpr int kKBytes = kBK * D * 2;
+    static constexpr int kStages = D == 64 ? 3 : 2;
+    static constexpr int kSmem = 1024 + kQBytes + kStages * kKBytes + 256;
+};
+
+template <int D>
+struct P2 {
+    static constexpr int kBK = 128, kBQ = 256;
+    static constexpr int kPanels = D / 64;
+    static constexpr int kKBytes = kBK * D * 2;
+    static constexpr int kAugA = 2 * kBK * 16;  // [ones pattern | zeros], 16 B rows
+    static constexpr int kQBytes = kBQ * D * 2;
+    static constexpr int kLBytes = kBQ * 16;
+    static constexpr int kStageBytes = kQBytes + kLBytes;
+    static constexpr int kStages = D == 64 ? 3 : 2;
+    static constexpr int kSmem = 1024 + kKBytes + kAugA + kStages * kStageBytes + 256;
+};
+
+// No-swizzle K-major descriptor: 8-row core matrices of 16 B rows (128 B
+// contiguous), SBO between 8-row groups, LBO between the two 8-element K halves.
+__device__ __forceinline__ uint64_t desc_noswz(const void* p, uint32_t lbo, uint32_t sbo) {
+    const uint64_t addr = smem_u32(p);
+    uint64_t d = 0;
+    d |= (addr >> 4) & 0x3FFFull;
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= 1ull << 46;  // version, layout type 0 = SWIZZLE_NONE
+    return d;
+}
+
+__device__ __forceinline__ __nv_bfloat16 f2bf(float x) { return __float2bfloat16_rn(x); }
+
+// ---------------------------------------------------------------- pass 1 --
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    score_lse_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk, int Hq, int Hkv,
+                     int Nq, int Nk, int causal, float c_log2, float* __restrict__ lse_out,
+                     __nv_bfloat16* __restrict__ lam_out) {
+    using C = P1<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;
+    uint8_t* sK = sQ + C::kQBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sK + C::kStages * C::kKBytes);
+    uint64_t* bar_q = bars;
+    uint64_t* k_full = bars + 1;
+    uint64_t* k_empty = k_full + C::kStages;
+    uint64_t* s_full = k_empty + C::kStages;
+    uint64_t* s_empty = s_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_empty + 2);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    const int q0 = blockIdx.x * C::kBQ, h = blockIdx.y, l = blockIdx.z;
+    const int g = Hq / Hkv;
+    const int qslab = l * Hq + h, kslab = l * Hkv + h / g;
+    const int off = Nk - Nq;  // causal: key j allowed iff j <= q + off
+    int n_kv = (Nk + C::kBK - 1) / C::kBK;
+    if (causal) {
+        const int last_key = q0 + C::kBQ - 1 + off;
+        const int t = last_key < 0 ? 0 : last_key / C::kBK + 1;
+        n_kv = t < n_kv ? t : n_kv;
+    }
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tq);
+        tma_prefetch(&tk);
+        mbar_init(bar_q, 1);
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(&k_full[s], 1);
+            mbar_init(&k_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&s_full[s], 1);
+            mbar_init(&s_empty[s], 4);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (elect_one() && n_kv > 0) {
+            mbar_arrive_expect_tx(bar_q, C::kQBytes);
+            for (int p = 0; p < C::kPanels; ++p) tma_load_3d(sQ + p * (C::kBQ * 128), &tq, bar_q, p * 64, q0, qslab);
+            for (int j = 0; j < n_kv; ++j) {
+                const int st = j % C::kStages;
+                mbar_wait(&k_empty[st], ((j / C::kStages) & 1) ^ 1);
+                mbar_arrive_expect_tx(&k_full[st], C::kKBytes);
+                uint8_t* dst = sK + st * C::kKBytes;
+                for (int p = 0; p < C::kPanels; ++p)
+                    tma_load_3d(dst + p * (C::kBK * 128), &tk, &k_full[st], p * 64, j * C::kBK, kslab);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc = idesc_f16(C::kBQ, C::kBK, 1);
+        if (n_kv > 0) mbar_wait(bar_q, 0);
+        for (int j = 0; j < n_kv; ++j) {
+            const int st = j % C::kStages, sb = j & 1;
+            mbar_wait(&k_full[st], (j / C::kStages) & 1);
+            mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+                for (int p = 0; p < C::kPanels; ++p) {
+                    const uint64_t a = desc_sw128(sQ + p * (C::kBQ * 128));
+                    const uint64_t b = desc_sw128(sK + st * C::kKBytes + p * (C::kBK * 128));
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) mma_f16_ss(tmem + sb * C::kBK, a + kk * 2, b + kk * 2, idesc, (p | kk) != 0);
+                }
+                mma_commit(&s_full[sb]);
+                mma_commit(&k_empty[st]);
+            }
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        const uint32_t quad = warp & 3;
+        const int r = quad * 32 + lane;
+        const int q = q0 + r;
+        const int kmax = causal ? (q + off + 1 < Nk ? q + off + 1 : Nk) : Nk;  // keys [0, kmax) allowed
+        float m = -INFINITY, lsum = 0.0f;
+        for (int j = 0; j < n_kv; ++j) {
+            const int sb = j & 1;
+            mbar_wait(&s_full[sb], (j >> 1) & 1);
+            tc_fence_after();
+            const uint32_t base = tmem + ((quad * 32) << 16) + sb * C::kBK;
+            const int valid = kmax - j * C::kBK;  // columns [0, valid) of this tile count
+#pragma unroll 1
+            for (int c0 = 0; c0 < C::kBK; c0 += 32) {
+                uint32_t rr[32];
+                tmem_ld32(base + c0, rr);
+                tmem_ld_wait();
+                float t[32];
+                float cm = -INFINITY;
+                if (valid >= c0 + 32) {
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) t[u] = __uint_as_float(rr[u]) * c_log2;
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) t[u] = (c0 + u < valid) ? __uint_as_float(rr[u]) * c_log2 : -INFINITY;
+                }
+#pragma unroll
+                for (int u = 0; u < 32; u += 2) cm = max3f(cm, t[u], t[u + 1]);
+                const float mn = fmaxf(m, cm);
+                if (mn == -INFINITY) continue;
+                float s = 0.0f;
+#pragma unroll
+                for (int u = 0; u < 32; ++u) s += ex2(t[u] - mn);
+                lsum = lsum * ex2(m - mn) + s;
+                m = mn;
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
+        }
+        if (q < Nq) {
+            const float lse2 = m + __log2f(lsum);  // log2 Σ exp2(c·s)
+            const int64_t row = (int64_t)qslab * Nq + q;
+            if (lse_out) lse_out[row] = lse2 / kLog2e;
+            if (lam_out) {
+                const float lam = lse2 / c_log2;  // √d · lse (raw-score units)
+                const __nv_bfloat16 hi = f2bf(lam);
+                const float r1 = lam - __bfloat162float(hi);
+                const __nv_bfloat16 mid = f2bf(r1);
+                const __nv_bfloat16 lo = f2bf(r1 - __bfloat162float(mid));
+                __align__(16) __nv_bfloat16 v[8];
+                v[0] = __hneg(hi);
+                v[1] = __hneg(mid);
+                v[2] = __hneg(lo);
+#pragma unroll
+                for (int u = 3; u < 8; ++u) v[u] = f2bf(0.0f);
+                *reinterpret_cast<uint4*>(lam_out + row * 8) = *reinterpret_cast<const uint4*>(v);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// λ rows from a caller-supplied natural-log LSE (proxy prefill).
+__global__ void lam_from_lse_kernel(const float* __restrict__ lse, int64_t rows, float sqrt_d,
+                                    __nv_bfloat16* __restrict__ lam_out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    const float lam = lse[i] * sqrt_d;
+    const __nv_bfloat16 hi = f2bf(lam);
+    const float r1 = lam - __bfloat162float(hi);
+    const __nv_bfloat16 mid = f2bf(r1);
+    const __nv_bfloat16 lo = f2bf(r1 - __bfloat162float(mid));
+    __align__(16) __nv_bfloat16 v[8];
+    v[0] = __hneg(hi);
+    v[1] = __hneg(mid);
+    v[2] = __hneg(lo);
+    for (int u = 3; u < 8; ++u) v[u] = f2bf(0.0f);
+    *reinterpret_cast<uint4*>(lam_out + i * 8) = *reinterpret_cast<const uint4*>(v);
+}
+
+// ---------------------------------------------------------------- pass 2 --
+template <int D, bool kMax>
+__global__ void __launch_bounds__(kThreads, 1)
+    score_pool_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                      const __grid_constant__ CUtensorMap tlam, int Hq, int Hkv, int Nq, int Nk, int causal,
+                      float c_log2, float* __restrict__ x_out) {
+    using C = P2<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sK = smem;
+    uint8_t* sAug = sK + C::kKBytes;
+    uint8_t* sQ = sAug + C::kAugA;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sQ + C::kStages * C::kStageBytes);
+    uint64_t* bar_k = bars;
+    uint64_t* q_full = bars + 1;
+    uint64_t* q_empty = q_full + C::kStages;
+    uint64_t* s_full = q_empty + C::kStages;
+    uint64_t* s_empty = s_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_empty + 2);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    const int k0 = blockIdx.x * C::kBK, kh = blockIdx.y, l = blockIdx.z;
+    const int g = Hq / Hkv;
+    const int kslab = l * Hkv + kh;
+    const int off = Nk - Nq;
+    const int tiles_per_head = (Nq + C::kBQ - 1) / C::kBQ;
+    // causal: query tiles whose last query still cannot see key k0 are skipped
+    int first_tile = 0;
+    if (causal) {
+        const int qmin = k0 - off;  // smallest query that sees key k0
+        first_tile = qmin <= 0 ? 0 : qmin / C::kBQ;
+        if (first_tile > tiles_per_head) first_tile = tiles_per_head;
+    }
+    const int tiles_h = tiles_per_head - first_tile;
+    const int n_tiles = g * tiles_h;
+
+    // K_aug: row r = [1, 1, 1, 0, 0, 0, 0, 0] then an all-zero K half.
+    for (int i = threadIdx.x; i < C::kAugA / 16; i += kThreads) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (i < C::kBK) {
+            const uint32_t one = 0x3F80u;  // bf16 1.0
+            v.x = one | (one << 16);
+            v.y = one;
+        }
+        reinterpret_cast<uint4*>(sAug)[i] = v;
+    }
+    fence_proxy_async_smem();
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tq);
+        tma_prefetch(&tk);
+        tma_prefetch(&tlam);
+        mbar_init(bar_k, 1);
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(&q_full[s], 1);
+            mbar_init(&q_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&s_full[s], 1);
+            mbar_init(&s_empty[s], 4);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (elect_one() && n_tiles > 0) {
+            mbar_arrive_expect_tx(bar_k, C::kKBytes);
+            for (int p = 0; p < C::kPanels; ++p) tma_load_3d(sK + p * (C::kBK * 128), &tk, bar_k, p * 64, k0, kslab);
+            for (int j = 0; j < n_tiles; ++j) {
+                const int st = j % C::kStages;
+                const int hh = j / tiles_h, qt = first_tile + j % tiles_h;
+                const int qslab = l * Hq + kh * g + hh;
+                mbar_wait(&q_empty[st], ((j / C::kStages) & 1) ^ 1);
+                mbar_arrive_expect_tx(&q_full[st], C::kStageBytes);
+                uint8_t* dst = sQ + st * C::kStageBytes;
+                for (int p = 0; p < C::kPanels; ++p)
+                    tma_load_3d(dst + p * (C::kBQ * 128), &tq, &q_full[st], p * 64, qt * C::kBQ, qslab);
+                tma_load_3d(dst + C::kQBytes, &tlam, &q_full[st], 0, qt * C::kBQ, qslab);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc = idesc_f16(C::kBK, C::kBQ, 1);
+        if (n_tiles > 0) mbar_wait(bar_k, 0);
+        for (int j = 0; j < n_tiles; ++j) {
+            const int st = j % C::kStages, sb = j & 1;
+            mbar_wait(&q_full[st], (j / C::kStages) & 1);
+            mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
+            tc_fence_after();
+            if (elect_one()) {
+                uint8_t* qs = sQ + st * C::kStageBytes;
+                const uint32_t d = tmem + sb * C::kBQ;
+#pragma unroll
+                for (int p = 0; p < C::kPanels; ++p) {
+                    const uint64_t a = desc_sw128(sK + p * (C::kBK * 128));
+                    const uint64_t b = desc_sw128(qs + p * (C::kBQ * 128));
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) mma_f16_ss(d, a + kk * 2, b + kk * 2, idesc, (p | kk) != 0);
+                }
+                // − λ_q: K_aug (ones, zero second K half via LBO) · Q_aug (−hi, −mid, −lo)
+                const uint64_t a_aug = desc_noswz(sAug, C::kBK * 16, 128);
+                const uint64_t b_aug = desc_noswz(qs + C::kQBytes, 0, 128);
+                mma_f16_ss(d, a_aug, b_aug, idesc, 1);
+                mma_commit(&s_full[sb]);
+                mma_commit(&q_empty[st]);
+            }
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        const uint32_t quad = warp & 3;
+        const int r = quad * 32 + lane;
+        const int key = k0 + r;
+        const int qmin = key - off;  // causal: queries >= qmin see this key
+        float acc = kMax ? -INFINITY : 0.0f;
+        for (int j = 0; j < n_tiles; ++j) {
+            const int sb = j & 1;
+            const int qbase = (first_tile + j % tiles_h) * C::kBQ;
+            int lo_col = causal ? qmin - qbase : 0;  // columns [lo_col, hi_col) valid
+            lo_col = lo_col < 0 ? 0 : lo_col;
+            const int hi_col = Nq - qbase < C::kBQ ? Nq - qbase : C::kBQ;
+            mbar_wait(&s_full[sb], (j >> 1) & 1);
+            tc_fence_after();
+            const uint32_t base = tmem + ((quad * 32) << 16) + sb * C::kBQ;
+            // tcgen05.ld is warp-collective: skip a chunk only if masked for every
+            // lane (lane 0 holds the warp's smallest key, hence smallest lo_col).
+            const int lo_warp = __shfl_sync(0xffffffffu, lo_col, 0);
+#pragma unroll 1
+            for (int c0 = 0; c0 < C::kBQ; c0 += 32) {
+                if (c0 >= hi_col || c0 + 32 <= lo_warp) continue;
+                uint32_t rr[32];
+                tmem_ld32(base + c0, rr);
+                tmem_ld_wait();
+                const bool full = c0 >= lo_col && c0 + 32 <= hi_col;
+                if (kMax) {
+                    if (full) {
+#pragma unroll
+                        for (int u = 0; u < 32; u += 2) acc = max3f(acc, __uint_as_float(rr[u]), __uint_as_float(rr[u + 1]));
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 32; ++u)
+                            if (c0 + u >= lo_col && c0 + u < hi_col) acc = fmaxf(acc, __uint_as_float(rr[u]));
+                    }
+                } else {
+                    float s = 0.0f;
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) {
+                        const float e = ex2(__uint_as_float(rr[u]) * c_log2);
+                        s += (full || (c0 + u >= lo_col && c0 + u < hi_col)) ? e : 0.0f;
+                    }
+                    acc += s;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
+        }
+        if (key < Nk) x_out[(int64_t)kslab * Nk + key] = kMax ? ex2(acc * c_log2) : acc;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+template <typename K>
+void set_smem(K kern, int bytes) {
+    PKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+template <int D>
+void run_lse(const ScoreShape& s, const void* q, const void* k, float* lse, __nv_bfloat16* lam, cudaStream_t st) {
+    using C = P1<D>;
+    static bool once = false;
+    if (!once) {
+        set_smem(score_lse_kernel<D>, C::kSmem);
+        once = true;
+    }
+    const CUtensorMap tq = make_tmap_3d(q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, s.Nq, s.L * s.Hq, D * 2, D * 2 * s.Nq,
+                                        64, C::kBQ, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+    const CUtensorMap tk = make_tmap_3d(k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, s.Nk, s.L * s.Hkv, D * 2, D * 2 * s.Nk,
+                                        64, C::kBK, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+    const dim3 grid((unsigned)((s.Nq + C::kBQ - 1) / C::kBQ), (unsigned)s.Hq, (unsigned)s.L);
+    score_lse_kernel<D><<<grid, kThreads, C::kSmem, st>>>(tq, tk, (int)s.Hq, (int)s.Hkv, (int)s.Nq, (int)s.Nk,
+                                                         s.causal ? 1 : 0, kLog2e / sqrtf((float)D), lse, lam);
+    check_launch("score_lse_kernel");
+}
+
+template <int D>
+void run_pool(const ScoreShape& s, const void* q, const void* k, const __nv_bfloat16* lam, bool reduce_max, float* x,
+              cudaStream_t st) {
+    using C = P2<D>;
+    static bool once = false;
+    if (!once) {
+        set_smem(score_pool_kernel<D, true>, C::kSmem);
+        set_smem(score_pool_kernel<D, false>, C::kSmem);
+        once = true;
+    }
+    const CUtensorMap tq = make_tmap_3d(q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, s.Nq, s.L * s.Hq, D * 2, D * 2 * s.Nq,
+                                        64, C::kBQ, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+    const CUtensorMap tk = make_tmap_3d(k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, s.Nk, s.L * s.Hkv, D * 2, D * 2 * s.Nk,
+                                        64, C::kBK, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+    const CUtensorMap tl = make_tmap_3d(lam, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 8, s.Nq, s.L * s.Hq, 16, 16 * s.Nq, 8,
+                                        C::kBQ, 1, CU_TENSOR_MAP_SWIZZLE_NONE);
+    const dim3 grid((unsigned)((s.Nk + C::kBK - 1) / C::kBK), (unsigned)s.Hkv, (unsigned)s.L);
+    const float c = kLog2e / sqrtf((float)D);
+    if (reduce_max) {
+        score_pool_kernel<D, true><<<grid, kThreads, C::kSmem, st>>>(tq, tk, tl, (int)s.Hq, (int)s.Hkv, (int)s.Nq,
+                                                                    (int)s.Nk, s.causal ? 1 : 0, c, x);
+    } else {
+        score_pool_kernel<D, false><<<grid, kThreads, C::kSmem, st>>>(tq, tk, tl, (int)s.Hq, (int)s.Hkv, (int)s.Nq,
+                                                                     (int)s.Nk, s.causal ? 1 : 0, c, x);
+    }
+    check_launch("score_pool_kernel");
+}
+
+}  // namespace
+
+void score_validate(const ScoreShape& s) {
+    PKV_REQUIRE_SHAPE(s.L > 0 && s.Hq > 0 && s.Hkv > 0 && s.Nq > 0 && s.Nk > 0, "score extents must be positive");
+    PKV_REQUIRE_SHAPE(s.Hq % s.Hkv == 0, "query heads ", s.Hq, " not a multiple of KV heads ", s.Hkv);
+    PKV_REQUIRE(s.d == 64 || s.d == 128, PKV_ECONFIG, "GPU scoring supports head_dim 64 or 128, got ", s.d);
+    PKV_REQUIRE(s.L * s.Hq <= 65535 && s.Nq < (int64_t(1) << 31) && s.Nk < (int64_t(1) << 31), PKV_ECONFIG,
+                "score shape too large for one launch");
+    PKV_REQUIRE(!s.causal || s.Nk >= s.Nq, PKV_ECONFIG, "causal scoring needs Nk >= Nq");
+}
+
+void launch_score_lse(const ScoreShape& s, const void* q, const void* k, float* lse, __nv_bfloat16* lam,
+                      cudaStream_t st) {
+    if (s.d == 64) run_lse<64>(s, q, k, lse, lam, st);
+    else run_lse<128>(s, q, k, lse, lam, st);
+}
+
+void launch_lam_from_lse(const float* lse, int64_t rows, int64_t d, __nv_bfloat16* lam, cudaStream_t st) {
+    lam_from_lse_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(lse, rows, sqrtf((float)d), lam);
+    check_launch("lam_from_lse_kernel");
+}
+
+void launch_score_pool(const ScoreShape& s, const void* q, const void* k, const __nv_bfloat16* lam, bool reduce_max,
+                       float* x, cudaStream_t st) {
+    if (s.d == 64) run_pool<64>(s, q, k, lam, reduce_max, x, st);
+    else run_pool<128>(s, q, k, lam, reduce_max, x, st);
+}
+
+}  // namespace pkv
