@@ -1,0 +1,449 @@
+#!/usr/bin/env python
+"""bench.py — ProxyKV pruning hot path on B200: score -> map -> select -> compact.
+
+Metric (BASELINE.json): proxy-scored+pruned tokens/s and prune latency at
+Llama-3.2-1B (proxy) -> Llama-3.1-8B (target) shapes, 32k context, 1 GPU
+(configs[1]); Top-K overlap is measured by the parity tests.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" = one full prune of one context: inputs (proxy Q, proxy K, target K/V)
+resident in HBM, outputs = packed K/V + retained indices. `value` = tokens/s
+over all ranks (weak scaling: every rank prunes its own context, no collective
+on the data path). `e2e` = the same through the C-ABI
+host-buffer call (pkv_pruner_run_host: H2D of inputs and D2H of outputs inside
+the timed region). `--impl reference` times the reference CPU implementation
+(oracle/_ref, the unmodified reference sources) on the host's cores on a
+bounded sample of the same workload and extrapolates to one context.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: proxy (L_s, Hq, H_s, dp), target (L_l, H_l, dt), N, rho
+    "llama32k": dict(Ls=16, Hq=32, Hs=8, dp=64, Ll=32, Hl=8, dt=128, N=32768, rho=0.2,
+                     desc="Llama-3.2-1B (16L,32Q/8KV,d64) proxy -> Llama-3.1-8B (32L,8KV,d128) target, 32k ctx"),
+    "tiny": dict(Ls=2, Hq=4, Hs=4, dp=64, Ll=4, Hl=8, dt=64, N=2048, rho=0.2,
+                 desc="tiny synthetic proxy(2L,4H,d64) -> target(4L,8H,d64), N=2048"),
+    "qwen25_128k": dict(Ls=24, Hq=14, Hs=2, dp=64, Ll=28, Hl=4, dt=128, N=131072, rho=0.2,
+                        desc="Qwen-2.5-0.5B (24L,14Q/2KV,d64) -> Qwen-2.5-7B (28L,4KV,d128), 128k ctx"),
+    "qwen3_64k": dict(Ls=28, Hq=16, Hs=8, dp=128, Ll=64, Hl=8, dt=128, N=65536, rho=0.2,
+                      desc="Qwen-3-0.6B (28L,16Q/8KV,d128) -> Qwen-3-32B (64L,8KV,d128), 64k ctx"),
+}
+METRIC = "proxy-scored+pruned tokens/s & prune latency (8B shapes, 32k ctx); Top-K overlap"
+UNIT = "tokens/s"
+
+
+# ------------------------------------------------------------ workload math --
+def windows(n, crop=2048, stride=1024):
+    if n <= crop:
+        return 1
+    w = (n - crop) // stride + 1
+    return w + (1 if (w - 1) * stride + crop < n else 0)
+
+
+def unique_pairs(Ll, Ls):
+    return len({(l * Ls + Ll - 1) // Ll for l in range(1, Ll + 1)})
+
+
+def flops_score_pass(c):
+    """2·d·Nq·Nk·Hq·L_s per pass (non-causal)."""
+    return 2 * c["dp"] * c["N"] * c["N"] * c["Hq"] * c["Ls"]
+
+
+def flops_mapper(c, D=512, enc=6, Dh=64):
+    """per-window algorithmic FLOPs of the reference mapper x U·W."""
+    nw = min(c["N"], 2048)
+    syn = c["Hs"]
+    per = (2 * nw * 256 * c["Hs"] * 3 + 2 * nw * 512 * 768 + enc * (24 * nw * D * D + 4 * nw * nw * D)
+           + 4 * nw * D * syn * Dh + 4 * nw * c["Hl"] * syn * Dh + 2 * nw * c["Hl"] * Dh)
+    return unique_pairs(c["Ll"], c["Ls"]) * windows(c["N"]) * per
+
+
+def k_of(c):
+    return math.ceil(c["rho"] * c["N"])
+
+
+def bytes_select(c):
+    s = c["Ll"] * c["Hl"]
+    return s * c["N"] * 4 + s * k_of(c) * 4
+
+
+def bytes_compact(c):
+    s = c["Ll"] * c["Hl"]
+    return 2 * s * k_of(c) * c["dt"] * 2 * 2 + s * k_of(c) * 4
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- our arm --
+def make_inputs(c, device, seed):
+    import torch
+    g = torch.Generator(device=device).manual_seed(seed)
+    Ls, Hq, Hs, dp, N = c["Ls"], c["Hq"], c["Hs"], c["dp"], c["N"]
+    q = torch.randn(Ls, Hq, N, dp, device=device, generator=g) * 0.35
+    kp = torch.randn(Ls, Hs, N, dp, device=device, generator=g)
+    u = torch.randn(dp, device=device, generator=g)
+    u = u / u.norm()
+    kp[:, :, : max(1, N // 50)] += 3.0 * u  # attention-sink structure
+    q += 0.8 * u
+    q, kp = q.to(torch.bfloat16), kp.to(torch.bfloat16)
+    kt = torch.randn(c["Ll"], c["Hl"], N, c["dt"], device=device, generator=g).to(torch.bfloat16)
+    vt = torch.randn(c["Ll"], c["Hl"], N, c["dt"], device=device, generator=g).to(torch.bfloat16)
+    return q, kp, kt, vt
+
+
+def time_loop(fn, iters, stream):
+    import torch
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(iters):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
+
+
+def run_ours(args, c, rank, world, local_rank):
+    import torch
+    import paper_2605_16360_b200 as P
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    ctx = P.Context(local_rank)
+    geom = P.ModelGeometry(c["Ll"], c["Hl"], c["Ls"], c["Hs"], c["dt"])
+    mcfg = P.MapperConfig()
+    mapper = P.Mapper(geom, mcfg, seed=7, precision=args.precision, ctx=ctx)
+    pr = P.Pruner(mapper, c["Hq"], c["dp"], c["dt"], c["N"], c["rho"])
+    K = pr.k
+    q, kp, kt, vt = make_inputs(c, dev, seed=1234 + rank)
+    ko = torch.empty(c["Ll"], c["Hl"], K, c["dt"], dtype=torch.bfloat16, device=dev)
+    vo = torch.empty_like(ko)
+    idx = torch.empty(c["Ll"], c["Hl"], K, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    step = lambda: pr.run(q, kp, kt, vt, ko, vo, idx, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = ctx.launches()
+    with ClockSampler(local_rank) as clk:
+        ms = time_loop(step, args.steps, stream)
+    launches = (ctx.launches() - l0) // max(args.steps, 1) * args.steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+        dist.barrier()
+
+    result = {"ms": ms, "K": K, "launches": launches, "clocks": clk.summary()}
+    if rank == 0:
+        result["stages"] = stage_breakdown(P, ctx, mapper, c, q, kp, kt, vt, ko, vo, K, stream, args)
+        if not args.no_e2e:
+            result["e2e"] = e2e(P, pr, c, K, args)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return result
+
+
+def stage_breakdown(P, ctx, mapper, c, q, kp, kt, vt, ko, vo, K, stream, args):
+    import torch
+    it = max(2, min(args.steps, 5))
+    lse = P.score_lse(q, kp, ctx=ctx)
+    x = torch.empty(c["Ls"], c["Hs"], c["N"], device=q.device)
+    y = torch.empty(1, c["Ll"], c["Hl"], c["N"], device=q.device)
+    idx = torch.empty(c["Ll"] * c["Hl"], K, dtype=torch.int32, device=q.device)
+    out = {}
+    out["score_lse_ms"] = time_loop(lambda: P.score_lse(q, kp, ctx=ctx, stream=stream), it, stream)
+    out["score_pool_ms"] = time_loop(lambda: P.score(q, kp, lse=lse, ctx=ctx, stream=stream, out=x), it, stream)
+    out["map_ms"] = time_loop(lambda: mapper.forward_full(x.view(1, *x.shape), stream=stream, out=y), it, stream)
+    ys = y.view(-1, c["N"])
+    out["select_ms"] = time_loop(lambda: P.topk_select(ys, K, want_mask=False, ctx=ctx, stream=stream), it, stream)
+    _, idx = P.topk_select(ys, K, want_mask=False, ctx=ctx, stream=stream)
+    S = c["Ll"] * c["Hl"]
+    out["compact_ms"] = time_loop(
+        lambda: P.compact_kv(kt.view(S, c["N"], c["dt"]), vt.view(S, c["N"], c["dt"]), idx, ctx=ctx, stream=stream,
+                             out=(ko.view(S, K, c["dt"]), vo.view(S, K, c["dt"]))), it, stream)
+    return out
+
+
+def e2e(P, pr, c, K, args):
+    import torch
+    q, kp, kt, vt = (t.cpu().pin_memory() for t in make_inputs(c, torch.device("cuda"), seed=99))
+    ko = torch.empty(c["Ll"], c["Hl"], K, c["dt"], dtype=torch.bfloat16).pin_memory()
+    vo = torch.empty_like(ko).pin_memory()
+    idx = torch.empty(c["Ll"], c["Hl"], K, dtype=torch.int32).pin_memory()
+    stream = torch.cuda.current_stream()
+    step = lambda: pr.run_host(q, kp, kt, vt, ko, vo, idx, stream=stream)
+    for _ in range(max(1, min(args.warmup, 2))):
+        step()
+    n = max(2, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(n):
+        step()  # synchronises on the stream at the end of every call
+    ms = (time.perf_counter() - t0) * 1e3 / n
+    h2d = sum(t.numel() * t.element_size() for t in (q, kp, kt, vt))
+    d2h = sum(t.numel() * t.element_size() for t in (ko, vo, idx))
+    return {"ms": ms, "h2d": h2d, "d2h": d2h}
+
+
+# ---------------------------------------------------------- reference arm --
+def cpu_reference_sample(c, threads, include_mapper=True):
+    """Times the reference CPU implementation on a bounded sample of one context
+    and extrapolates to the full context (seconds per context, per stage).
+      select+indices: reference topk_mask + apply_mask on one full target layer
+                      (H_l slices of N), x L_l layers;
+      compaction:     (no reference code) C restatement gather of one layer, x L_l;
+      mapper:         reference forward_pair on one 2048-window per thread, run
+                      concurrently on `threads` cores, x ceil(U·W / threads);
+      scoring:        (SPEC-only, no reference code) fp64 C restatement on one
+                      (layer, KV head) with 256 queries per thread, scaled by
+                      the full query count, heads and layers."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import pkv_oracle as O
+
+    ref = O.RefLib()
+    N, Ll, Hl, dt = c["N"], c["Ll"], c["Hl"], c["dt"]
+    r = np.random.RandomState(0)
+    out = {}
+    # select + apply_mask, one target layer
+    s = r.rand(1, 1, Hl, N)
+    t0 = time.perf_counter()
+    bits, k = ref.topk_mask(s, c["rho"])
+    ref.apply_mask(bits, k, dt)
+    out["select"] = (time.perf_counter() - t0) * Ll
+    # compaction, one target layer (C restatement; the reference has no gather)
+    kb = r.randint(0, 1 << 15, (Hl, N, dt)).astype(np.uint16)
+    _, idx = O.topk_select(s.reshape(Hl, N).astype(np.float32), k)
+    t0 = time.perf_counter()
+    O.compact_kv(kb, kb, idx)
+    out["compact"] = (time.perf_counter() - t0) * Ll
+    # scoring: `threads` concurrent (layer, kv-head) samples of 256 queries of one head group
+    g = c["Hq"] // c["Hs"]
+    nq = 256
+    qb = O.f32_to_bf16_bits(r.standard_normal((1, g, nq, c["dp"])).astype(np.float32))
+    kk = O.f32_to_bf16_bits(r.standard_normal((1, 1, N, c["dp"])).astype(np.float32))
+
+    def one_score(_):
+        O.score(qb, kk, reduce="max")
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(one_score, range(threads)))
+    ts = time.perf_counter() - t0
+    units = (N / nq) * c["Ls"] * c["Hs"]  # (layer, kv head, 256-query block) units per context
+    out["score"] = ts * units / threads
+    if include_mapper:
+        geo = O.Geometry(Ll, Hl, c["Ls"], c["Hs"], dt)
+        m = ref.mapper(geo, O.MapperConfig(), 7)
+        x = r.uniform(0, 2, (1, c["Hs"], min(N, 2048)))
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda _: m.forward_pair(x), range(threads)))
+        tm = time.perf_counter() - t0
+        n_win = unique_pairs(Ll, c["Ls"]) * windows(N)
+        out["map"] = tm * math.ceil(n_win / threads)
+    return out
+
+
+def cpu_sample_desc(c, threads):
+    return (f"reference topk_mask+apply_mask on 1 of {c['Ll']} target layers (x{c['Ll']}); reference forward_pair on "
+            f"{threads} concurrent 2048-windows (x ceil({unique_pairs(c['Ll'], c['Ls'])}*{windows(c['N'])}/{threads})); "
+            f"fp64 C-restatement scoring of {threads} (layer,kv-head,256-query) blocks and gather of 1 layer "
+            f"(no reference code for those), extrapolated to one {c['N']}-token context")
+
+
+def run_reference(args, c):
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):  # warm-up: the cheap stages only
+        cpu_reference_sample(c, threads, include_mapper=False)
+    totals = []
+    for _ in range(args.steps):
+        st = cpu_reference_sample(c, threads)
+        totals.append(sum(st.values()))
+    sec = statistics.mean(totals)
+    value = c["N"] / sec
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "desc": c["desc"], "rho": c["rho"], "N": c["N"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": cpu_sample_desc(c, threads), "stage_s": st},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+# -------------------------------------------------------------------- main --
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="llama32k")
+    ap.add_argument("--precision", type=int, default=3, help="mapper precision mode (1 fp16, 2 act split, 3 act+wt split)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    c = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+
+    if args.impl == "reference":
+        if rank == 0:
+            try:
+                print(json.dumps(run_reference(args, c)))
+            except Exception as e:  # noqa: BLE001
+                print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}))
+        return
+
+    r = run_ours(args, c, rank, world, local_rank)
+    if rank != 0:
+        return
+    hbm, tf_burst, tf_sus, src = peaks()
+    ms = r["ms"]
+    st = r["stages"]
+    # dominant kernel by stage time
+    tensor_stages = {"score_lse_ms": flops_score_pass(c), "score_pool_ms": flops_score_pass(c),
+                     "map_ms": flops_mapper(c)}
+    dom = max(st, key=lambda k: st[k])
+    if dom in tensor_stages:
+        ach = tensor_stages[dom] / (st[dom] * 1e-3) / 1e12
+        roof = {"kernel": dom[:-3], "bound": "tensor", "achieved": ach, "peak": tf_burst, "unit": "TFLOP/s",
+                "frac": ach / tf_burst, "traffic": None, "peak_source": f"{src} bf16 burst"}
+    else:
+        b = bytes_select(c) if dom == "select_ms" else bytes_compact(c)
+        ach = b / (st[dom] * 1e-3) / 1e9
+        roof = {"kernel": dom[:-3], "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": None, "peak_source": f"{src} hbm"}
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        roof["traffic"] = json.load(open(prof)).get(roof["kernel"])
+    sc_b = bytes_select(c) + bytes_compact(c)
+    sc_ms = st["select_ms"] + st["compact_ms"]
+    stage_roof = {
+        "score_lse": {"TFLOP/s": flops_score_pass(c) / st["score_lse_ms"] / 1e9},
+        "score_pool": {"TFLOP/s": flops_score_pass(c) / st["score_pool_ms"] / 1e9},
+        "map": {"TFLOP/s": flops_mapper(c) / st["map_ms"] / 1e9},
+        "select+compact": {"GB/s": sc_b / sc_ms / 1e6, "frac_hbm": sc_b / sc_ms / 1e6 / hbm},
+    }
+    line = {
+        "metric": METRIC, "value": c["N"] * world / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": args.config, "desc": c["desc"], "rho": c["rho"], "N": c["N"], "K": r["K"],
+                   "mapper_precision": args.precision, "score_reduce": "max", "score_passes": 2,
+                   "l2": "inputs (7 GB) > L2 (126 MB); no explicit flush",
+                   "parallelism": f"weak: {world} independent contexts, one per GPU"},
+        "prune_latency_ms": ms,
+        "stages_ms": {k[:-3]: v for k, v in st.items()},
+        "stage_roofline": stage_roof,
+        "roofline": roof,
+        "clocks": r["clocks"],
+        "gpu_launches": r["launches"],
+    }
+    if "e2e" in r:
+        e = r["e2e"]
+        line["e2e"] = {"value": c["N"] / (e["ms"] * 1e-3), "unit": UNIT, "h2d_bytes_per_step": e["h2d"],
+                       "d2h_bytes_per_step": e["d2h"], "ms_per_step": e["ms"]}
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            threads = os.cpu_count() or 1
+            stc = cpu_reference_sample(c, threads)
+            sec = sum(stc.values())
+            line["cpu_baseline"] = {"value": c["N"] / sec, "unit": UNIT, "cores": threads, "kind": "reference",
+                                    "sample": cpu_sample_desc(c, threads),
+                                    "stage_s": {k: round(v, 3) for k, v in stc.items()}}
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "unavailable": f"{type(e).__name__}: {e}"}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

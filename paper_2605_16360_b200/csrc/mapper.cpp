@@ -607,10 +607,6 @@ void Mapper::run(const float* x, const std::vector<int64_t>& unit_off, int64_t N
 
 using namespace pkv;
 
-struct pkv_mapper_s {
-    std::unique_ptr<Mapper> m;
-};
-
 extern "C" {
 
 pkv_status pkv_layer_pair(int64_t target_layer, const int64_t* geom5, int64_t* out) {

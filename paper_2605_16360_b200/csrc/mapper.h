@@ -79,3 +79,7 @@ private:
 };
 
 }  // namespace pkv
+
+struct pkv_mapper_s {
+    std::unique_ptr<pkv::Mapper> m;
+};
