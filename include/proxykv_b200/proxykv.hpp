@@ -1,0 +1,195 @@
+// proxykv.hpp — header-only C++ drop-in over the C ABI (pkv_capi.h) with the
+// reference's scoring / mapper / prune signatures and exception taxonomy
+// (proj/include/proxykv/{common,pruning,mapper}.hpp). A reference caller swaps
+//   #include "proxykv/pruning.hpp"          ->  #include "proxykv_b200/proxykv.hpp"
+//   proxykv::topk_mask(scores, rho)         ->  proxykv_b200::topk_mask(ctx, scores, rho)
+// and links libpkv_b200.so. Host containers here are plain std::vector (the
+// reference Tensor is an autodiff node; only its shape + row-major fp64 data
+// cross the boundary).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../pkv_capi.h"
+
+namespace proxykv_b200 {
+
+// common.hpp:13-52
+struct Error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ShapeError : Error {
+    using Error::Error;
+};
+struct ValueError : Error {
+    using Error::Error;
+};
+struct ConfigError : Error {
+    using Error::Error;
+};
+struct CudaError : Error {
+    using Error::Error;
+};
+struct NoDeviceError : Error {
+    using Error::Error;
+};
+
+inline void check(pkv_status s) {
+    if (s == PKV_OK) return;
+    const std::string msg = pkv_last_error();
+    switch (s) {
+        case PKV_ESHAPE: throw ShapeError(msg);
+        case PKV_EVALUE: throw ValueError(msg);
+        case PKV_ECONFIG: throw ConfigError(msg);
+        case PKV_ENODEV: throw NoDeviceError(msg);
+        default: throw CudaError(msg);
+    }
+}
+
+class Context {
+public:
+    explicit Context(int device = 0) { check(pkv_ctx_create(device, &h_)); }
+    ~Context() { pkv_ctx_destroy(h_); }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+    pkv_ctx get() const { return h_; }
+
+private:
+    pkv_ctx h_ = nullptr;
+};
+
+using Shape = std::vector<int64_t>;
+
+// pruning.hpp:14
+inline int64_t retention_count(double rho, int64_t n) {
+    int64_t k = 0;
+    check(pkv_retention_count(rho, n, &k));
+    return k;
+}
+
+// pruning.hpp:22-30
+struct PruneMask {
+    Shape shape;
+    std::vector<uint8_t> bits;
+    double retention_ratio = 1.0;
+    int64_t k = 0;
+    int64_t token_count() const { return shape.back(); }
+    int64_t slice_count() const {
+        int64_t n = 1;
+        for (int64_t e : shape) n *= e;
+        return n / shape.back();
+    }
+};
+
+// pruning.hpp:32 / pruning.cpp:37-56 — scores row-major fp64 (fp32-representable
+// for bit-exact parity), last axis = tokens. Runs the GPU radix select.
+inline PruneMask topk_mask(const Context& ctx, const std::vector<double>& scores, const Shape& shape, double rho) {
+    if (shape.empty()) throw ShapeError("topk_mask needs a shaped tensor");
+    PruneMask m;
+    m.shape = shape;
+    m.retention_ratio = rho;
+    m.bits.assign(scores.size(), 0);
+    const int64_t n = shape.back();
+    check(pkv_topk_mask_host(ctx.get(), scores.data(), static_cast<int64_t>(scores.size()) / n, n, rho,
+                             m.bits.data(), &m.k));
+    return m;
+}
+
+// pruning.hpp:48-53, 57 / pruning.cpp:197-215
+struct MaskApplication {
+    std::vector<std::vector<int64_t>> retained;
+    int64_t dropped_per_slice = 0;
+    int64_t bytes_saved_per_head = 0;
+    int64_t bytes_saved_total = 0;
+};
+
+inline MaskApplication apply_mask(const PruneMask& mask, int64_t head_dim, int64_t bytes_per_elem = 2) {
+    MaskApplication a;
+    const int64_t n = mask.token_count(), slices = mask.slice_count();
+    a.retained.resize(static_cast<size_t>(slices));
+    for (int64_t s = 0; s < slices; ++s) {
+        auto& l = a.retained[static_cast<size_t>(s)];
+        l.reserve(static_cast<size_t>(mask.k));
+        for (int64_t i = 0; i < n; ++i)
+            if (mask.bits[static_cast<size_t>(s * n + i)]) l.push_back(i);
+    }
+    a.dropped_per_slice = n - mask.k;
+    a.bytes_saved_per_head = a.dropped_per_slice * head_dim * bytes_per_elem * 2;
+    a.bytes_saved_total = a.bytes_saved_per_head * slices;
+    return a;
+}
+
+// mapper.hpp:16-25 / 35-55
+struct ModelGeometry {
+    int64_t target_layers = 32, target_heads = 32, proxy_layers = 16, proxy_heads = 32, head_dim = 128;
+    std::vector<int64_t> as5() const { return {target_layers, target_heads, proxy_layers, proxy_heads, head_dim}; }
+};
+
+enum class StageMode { kActive, kBypass };
+
+struct MapperConfig {
+    int64_t d_time = 512, encoder_layers = 6, encoder_heads = 8, ffn_mult = 4, d_head = 64, crop_len = 2048,
+            stride = 1024, synthetic_heads = 0;
+    StageMode stage_conv = StageMode::kActive, stage_encoder = StageMode::kActive, stage_cross = StageMode::kActive;
+    bool normalize_input = false;
+    std::vector<int64_t> as12() const {
+        auto m = [](StageMode s) { return s == StageMode::kBypass ? int64_t(1) : int64_t(0); };
+        return {d_time, encoder_layers, encoder_heads, ffn_mult, d_head, crop_len, stride, synthetic_heads,
+                m(stage_conv), m(stage_encoder), m(stage_cross), normalize_input ? 1 : 0};
+    }
+};
+
+// mapper.hpp:58, 65
+inline int64_t layer_pair(int64_t target_layer, const ModelGeometry& g) {
+    int64_t out = 0;
+    check(pkv_layer_pair(target_layer, g.as5().data(), &out));
+    return out;
+}
+
+inline std::vector<int64_t> window_offsets(int64_t n, int64_t crop, int64_t stride) {
+    int64_t cnt = 0;
+    check(pkv_window_offsets(n, crop, stride, nullptr, 0, &cnt));
+    std::vector<int64_t> v(static_cast<size_t>(cnt));
+    check(pkv_window_offsets(n, crop, stride, v.data(), cnt, &cnt));
+    return v;
+}
+
+// mapper.hpp:94 MapperParams::init -> flat fp64 blob (named_parameters + named_buffers)
+inline std::vector<double> mapper_init_params(const ModelGeometry& g, const MapperConfig& c, uint64_t seed) {
+    int64_t n = 0;
+    check(pkv_mapper_init_params(g.as5().data(), c.as12().data(), seed, nullptr, &n));
+    std::vector<double> blob(static_cast<size_t>(n));
+    check(pkv_mapper_init_params(g.as5().data(), c.as12().data(), seed, blob.data(), &n));
+    return blob;
+}
+
+// Device-resident mapper; forward_full takes/returns DEVICE fp32 buffers
+// (mapper.hpp:126; the host-tensor form is a cudaMemcpy on either side).
+class Mapper {
+public:
+    Mapper(const Context& ctx, const ModelGeometry& g, const MapperConfig& c, const std::vector<double>& blob,
+           uint32_t precision = PKV_MAPPER_FP16X3)
+        : geom_(g) {
+        check(pkv_mapper_create(ctx.get(), g.as5().data(), c.as12().data(), blob.data(),
+                                static_cast<int64_t>(blob.size()), precision, &h_));
+    }
+    ~Mapper() { pkv_mapper_destroy(h_); }
+    Mapper(const Mapper&) = delete;
+    Mapper& operator=(const Mapper&) = delete;
+    void forward_full(const float* x_all_dev, int64_t B, int64_t N, float* y_all_dev, void* stream = nullptr) {
+        check(pkv_mapper_forward_full(h_, x_all_dev, B, N, y_all_dev, stream));
+    }
+    void sliding_forward(const float* x_dev, int64_t B, int64_t N, float* y_dev, void* stream = nullptr) {
+        check(pkv_mapper_sliding_forward(h_, x_dev, B, N, y_dev, stream));
+    }
+    pkv_mapper get() const { return h_; }
+
+private:
+    pkv_mapper h_ = nullptr;
+    ModelGeometry geom_;
+};
+
+}  // namespace proxykv_b200

@@ -266,6 +266,7 @@ template <int BN>
 void dispatch_planes(const GemmArgs& g, int sm, cudaStream_t st) {
     if (g.na == 1 && g.nb == 1) return dispatch_epi<BN, 1, 1>(g, sm, st);
     if (g.na == 2 && g.nb == 1) return dispatch_epi<BN, 2, 1>(g, sm, st);
+    if (g.na == 1 && g.nb == 2) return dispatch_epi<BN, 1, 2>(g, sm, st);
     if (g.na == 2 && g.nb == 2) return dispatch_epi<BN, 2, 2>(g, sm, st);
     throw Error{PKV_ECONFIG, cat("unsupported GEMM plane combination na=", g.na, " nb=", g.nb)};
 }

@@ -277,9 +277,9 @@ Mapper::Mapper(pkv_ctx c, const Geometry& g, const Config& cf, const double* blo
     : ctx(c), geom(g), cfg(cf) {
     geom.validate();
     cfg.validate();
-    PKV_REQUIRE(precision >= 1 && precision <= 3, PKV_ECONFIG, "unknown mapper precision mode ", precision);
-    na = precision >= 2 ? 2 : 1;
-    nb = precision == 3 ? 2 : 1;
+    PKV_REQUIRE(precision >= 1 && precision <= 4, PKV_ECONFIG, "unknown mapper precision mode ", precision);
+    na = (precision == 2 || precision == 3) ? 2 : 1;
+    nb = (precision == 3 || precision == 4) ? 2 : 1;
     const int64_t D = cfg.d_time;
     PKV_REQUIRE(D % 128 == 0 && D <= 1024, PKV_ECONFIG, "GPU mapper needs d_time % 128 == 0 and <= 1024, got ", D);
     if (cfg.enc_active && cfg.encoder_layers > 0) {

@@ -3,13 +3,17 @@
 // style on tcgen05 so the N_q×N_k attention matrix is never materialised:
 //
 //   pass 1 (score_lse_kernel):  S = Q·Kᵀ (M = 128 queries, N = 256 keys) into
-//     TMEM; one thread per query row keeps an online (max, Σexp2) in registers;
-//     writes lse[q] and the bf16 triple (hi, mid, lo) of λ_q = √d·lse_q.
-//   pass 2 (score_pool_kernel): Sᵀ' = K·Qᵀ − λ (M = 128 keys, N = 256 queries),
-//     the −λ_q column folded into the MMA as 3 extra K columns (K_aug = 1,
-//     Q_aug = −(hi, mid, lo)); one thread per key row reduces over queries in
-//     registers: max mode = one FMNMX per element (max_q P = exp2(c·max_q S'),
-//     c = log2(e)/√d); sum mode = exp2 + FADD per element.
+//     double-buffered TMEM; 16 softmax warps (4 column segments x 4 TMEM lane
+//     quadrants) keep an online (max, Σexp2) per row segment in registers,
+//     merged through smem at the end; 1 in 4 exponentials is evaluated as a
+//     degree-4 polynomial on the FMA pipe to offload MUFU (FA4-style); writes
+//     lse[q] and the bf16 triple (hi, mid, lo) of λ_q = √d·lse_q.
+//   pass 2 (score_pool_kernel): S' = K·Qᵀ − λ (two M = 128 key blocks = 256
+//     keys per CTA, N = 128 queries per tile), the −λ_q column folded into the
+//     MMA as 3 extra K columns (K_aug = 1, Q_aug = −(hi, mid, lo)); one thread
+//     per key row reduces over queries in registers: max mode = one FMNMX3 per
+//     2 elements (max_q P = exp2(c·max_q S'), c = log2(e)/√d); sum mode =
+//     exp2 + FADD per element.
 // GQA: pass 2 walks the queries of all heads of a KV head's group.
 //
 // q bf16 [L, Hq, Nq, d], k bf16 [L, Hkv, Nk, d]; d ∈ {64, 128}.
@@ -21,30 +25,33 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kThreads = 256;
 constexpr float kLog2e = 1.4426950408889634f;
 
 template <int D>
 struct P1 {
     static constexpr int kBQ = 128, kBK = 256;
+    static constexpr int kSegs = 4;  // column segments of 64
+    static constexpr int kSoftWarps = 4 * kSegs;
+    static constexpr int kThreads = 128 + 32 * kSoftWarps;
     static constexpr int kPanels = D / 64;
     static constexpr int kQBytes = kBQ * D * 2;
     static constexpr int kKBytes = kBK * D * 2;
     static constexpr int kStages = D == 64 ? 3 : 2;
-    static constexpr int kSmem = 1024 + kQBytes + kStages * kKBytes + 256;
+    static constexpr int kSmem = 1024 + kQBytes + kStages * kKBytes + 256 + kSegs * kBQ * 8;
 };
 
 template <int D>
 struct P2 {
-    static constexpr int kBK = 128, kBQ = 256;
+    static constexpr int kBK = 128, kBlocks = 2, kBQ = 128;
+    static constexpr int kThreads = 128 + 32 * 4 * kBlocks;
     static constexpr int kPanels = D / 64;
-    static constexpr int kKBytes = kBK * D * 2;
+    static constexpr int kKBytes = kBK * D * 2;  // per key block
     static constexpr int kAugA = 2 * kBK * 16;  // [ones pattern | zeros], 16 B rows
     static constexpr int kQBytes = kBQ * D * 2;
     static constexpr int kLBytes = kBQ * 16;
     static constexpr int kStageBytes = kQBytes + kLBytes;
-    static constexpr int kStages = D == 64 ? 3 : 2;
-    static constexpr int kSmem = 1024 + kKBytes + kAugA + kStages * kStageBytes + 256;
+    static constexpr int kStages = D == 64 ? 4 : 3;
+    static constexpr int kSmem = 1024 + kBlocks * kKBytes + kAugA + kStages * kStageBytes + 256;
 };
 
 // No-swizzle K-major descriptor: 8-row core matrices of 16 B rows (128 B
@@ -59,11 +66,23 @@ __device__ __forceinline__ uint64_t desc_noswz(const void* p, uint32_t lbo, uint
     return d;
 }
 
-__device__ __forceinline__ __nv_bfloat16 f2bf(float x) { return __float2bfloat16_rn(x); }
+__device__ __forceinline__ void write_lam(__nv_bfloat16* dst, float lam) {
+    const __nv_bfloat16 hi = __float2bfloat16_rn(lam);
+    const float r1 = lam - __bfloat162float(hi);
+    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+    __align__(16) __nv_bfloat16 v[8];
+    v[0] = __hneg(hi);
+    v[1] = __hneg(mid);
+    v[2] = __hneg(lo);
+#pragma unroll
+    for (int u = 3; u < 8; ++u) v[u] = __float2bfloat16_rn(0.0f);
+    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
+}
 
 // ---------------------------------------------------------------- pass 1 --
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(P1<D>::kThreads, 1)
     score_lse_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk, int Hq, int Hkv,
                      int Nq, int Nk, int causal, float c_log2, float* __restrict__ lse_out,
                      __nv_bfloat16* __restrict__ lam_out) {
@@ -79,6 +98,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* s_full = k_empty + C::kStages;
     uint64_t* s_empty = s_full + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_empty + 2);
+    float2* part = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [segs][128] (m, l)
 
     const uint32_t warp = warp_id(), lane = lane_id();
     const int q0 = blockIdx.x * C::kBQ, h = blockIdx.y, l = blockIdx.z;
@@ -102,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&s_full[s], 1);
-            mbar_init(&s_empty[s], 4);
+            mbar_init(&s_empty[s], C::kSoftWarps);
         }
         fence_barrier_init();
     }
@@ -139,7 +159,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint64_t a = desc_sw128(sQ + p * (C::kBQ * 128));
                     const uint64_t b = desc_sw128(sK + st * C::kKBytes + p * (C::kBK * 128));
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) mma_f16_ss(tmem + sb * C::kBK, a + kk * 2, b + kk * 2, idesc, (p | kk) != 0);
+                    for (int kk = 0; kk < 4; ++kk)
+                        mma_f16_ss(tmem + sb * C::kBK, a + kk * 2, b + kk * 2, idesc, (p | kk) != 0);
                 }
                 mma_commit(&s_full[sb]);
                 mma_commit(&k_empty[st]);
@@ -148,62 +169,66 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= 4) {
         const uint32_t quad = warp & 3;
+        const int seg = (warp - 4) >> 2;  // 64-column segment of the 256-key tile
         const int r = quad * 32 + lane;
         const int q = q0 + r;
         const int kmax = causal ? (q + off + 1 < Nk ? q + off + 1 : Nk) : Nk;  // keys [0, kmax) allowed
-        float m = -INFINITY, lsum = 0.0f;
+        float m = -INFINITY, lsum = 0.0f;  // m in the log2 (scaled) domain
         for (int j = 0; j < n_kv; ++j) {
             const int sb = j & 1;
             mbar_wait(&s_full[sb], (j >> 1) & 1);
             tc_fence_after();
-            const uint32_t base = tmem + ((quad * 32) << 16) + sb * C::kBK;
-            const int valid = kmax - j * C::kBK;  // columns [0, valid) of this tile count
-#pragma unroll 1
-            for (int c0 = 0; c0 < C::kBK; c0 += 32) {
-                uint32_t rr[32];
-                tmem_ld32(base + c0, rr);
-                tmem_ld_wait();
-                float t[32];
-                float cm = -INFINITY;
-                if (valid >= c0 + 32) {
-#pragma unroll
-                    for (int u = 0; u < 32; ++u) t[u] = __uint_as_float(rr[u]) * c_log2;
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 32; ++u) t[u] = (c0 + u < valid) ? __uint_as_float(rr[u]) * c_log2 : -INFINITY;
-                }
-#pragma unroll
-                for (int u = 0; u < 32; u += 2) cm = max3f(cm, t[u], t[u + 1]);
-                const float mn = fmaxf(m, cm);
-                if (mn == -INFINITY) continue;
-                float s = 0.0f;
-#pragma unroll
-                for (int u = 0; u < 32; ++u) s += ex2(t[u] - mn);
-                lsum = lsum * ex2(m - mn) + s;
-                m = mn;
-            }
+            const uint32_t base = tmem + ((quad * 32) << 16) + sb * C::kBK + seg * 64;
+            uint32_t ra[32], rb[32];
+            tmem_ld32(base, ra);
+            tmem_ld32(base + 32, rb);
+            tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[sb]);
+            const int valid = kmax - (j * C::kBK + seg * 64);  // columns [0, valid) of this segment count
+            float v[64];
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+                v[u] = __uint_as_float(ra[u]);
+                v[32 + u] = __uint_as_float(rb[u]);
+            }
+            if (valid < 64) {
+#pragma unroll
+                for (int u = 0; u < 64; ++u) v[u] = (u < valid) ? v[u] : -INFINITY;
+            }
+            float cm = -INFINITY;
+#pragma unroll
+            for (int u = 0; u < 64; u += 2) cm = max3f(cm, v[u], v[u + 1]);
+            const float mn = fmaxf(m, cm * c_log2);
+            if (mn == -INFINITY) continue;
+            float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
+#pragma unroll
+            for (int u = 0; u < 64; u += 4) {
+                s0 += ex2(fmaf(v[u], c_log2, -mn));
+                s1 += ex2(fmaf(v[u + 1], c_log2, -mn));
+                s2 += ex2(fmaf(v[u + 2], c_log2, -mn));
+                s3 += ex2_poly(fmaf(v[u + 3], c_log2, -mn));
+            }
+            lsum = lsum * ex2(m - mn) + ((s0 + s1) + (s2 + s3));
+            m = mn;
         }
-        if (q < Nq) {
-            const float lse2 = m + __log2f(lsum);  // log2 Σ exp2(c·s)
+        part[seg * C::kBQ + r] = make_float2(m, lsum);
+        named_bar_sync(1, 32 * C::kSoftWarps);
+        if (seg == 0 && q < Nq) {
+            float M = -INFINITY;
+#pragma unroll
+            for (int s = 0; s < C::kSegs; ++s) M = fmaxf(M, part[s * C::kBQ + r].x);
+            float L = 0.0f;
+#pragma unroll
+            for (int s = 0; s < C::kSegs; ++s) {
+                const float2 pm = part[s * C::kBQ + r];
+                L += pm.y * ex2(pm.x - M);
+            }
+            const float lse2 = M + __log2f(L);  // log2 Σ exp2(c·s)
             const int64_t row = (int64_t)qslab * Nq + q;
             if (lse_out) lse_out[row] = lse2 / kLog2e;
-            if (lam_out) {
-                const float lam = lse2 / c_log2;  // √d · lse (raw-score units)
-                const __nv_bfloat16 hi = f2bf(lam);
-                const float r1 = lam - __bfloat162float(hi);
-                const __nv_bfloat16 mid = f2bf(r1);
-                const __nv_bfloat16 lo = f2bf(r1 - __bfloat162float(mid));
-                __align__(16) __nv_bfloat16 v[8];
-                v[0] = __hneg(hi);
-                v[1] = __hneg(mid);
-                v[2] = __hneg(lo);
-#pragma unroll
-                for (int u = 3; u < 8; ++u) v[u] = f2bf(0.0f);
-                *reinterpret_cast<uint4*>(lam_out + row * 8) = *reinterpret_cast<const uint4*>(v);
-            }
+            if (lam_out) write_lam(lam_out + row * 8, lse2 / c_log2);  // √d·lse (raw-score units)
         }
     }
     tc_fence_before();
@@ -219,30 +244,20 @@ __global__ void lam_from_lse_kernel(const float* __restrict__ lse, int64_t rows,
                                     __nv_bfloat16* __restrict__ lam_out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= rows) return;
-    const float lam = lse[i] * sqrt_d;
-    const __nv_bfloat16 hi = f2bf(lam);
-    const float r1 = lam - __bfloat162float(hi);
-    const __nv_bfloat16 mid = f2bf(r1);
-    const __nv_bfloat16 lo = f2bf(r1 - __bfloat162float(mid));
-    __align__(16) __nv_bfloat16 v[8];
-    v[0] = __hneg(hi);
-    v[1] = __hneg(mid);
-    v[2] = __hneg(lo);
-    for (int u = 3; u < 8; ++u) v[u] = f2bf(0.0f);
-    *reinterpret_cast<uint4*>(lam_out + i * 8) = *reinterpret_cast<const uint4*>(v);
+    write_lam(lam_out + i * 8, lse[i] * sqrt_d);
 }
 
 // ---------------------------------------------------------------- pass 2 --
 template <int D, bool kMax>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(P2<D>::kThreads, 1)
     score_pool_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                       const __grid_constant__ CUtensorMap tlam, int Hq, int Hkv, int Nq, int Nk, int causal,
                       float c_log2, float* __restrict__ x_out) {
     using C = P2<D>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sK = smem;
-    uint8_t* sAug = sK + C::kKBytes;
+    uint8_t* sK = smem;  // [blocks][panels][128 rows x 128 B]
+    uint8_t* sAug = sK + C::kBlocks * C::kKBytes;
     uint8_t* sQ = sAug + C::kAugA;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sQ + C::kStages * C::kStageBytes);
     uint64_t* bar_k = bars;
@@ -253,15 +268,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_empty + 2);
 
     const uint32_t warp = warp_id(), lane = lane_id();
-    const int k0 = blockIdx.x * C::kBK, kh = blockIdx.y, l = blockIdx.z;
+    const int k0 = blockIdx.x * (C::kBK * C::kBlocks), kh = blockIdx.y, l = blockIdx.z;
     const int g = Hq / Hkv;
     const int kslab = l * Hkv + kh;
     const int off = Nk - Nq;
     const int tiles_per_head = (Nq + C::kBQ - 1) / C::kBQ;
-    // causal: query tiles whose last query still cannot see key k0 are skipped
+    // causal: query tiles whose every query is earlier than k0 - off are skipped
     int first_tile = 0;
     if (causal) {
-        const int qmin = k0 - off;  // smallest query that sees key k0
+        const int qmin = k0 - off;
         first_tile = qmin <= 0 ? 0 : qmin / C::kBQ;
         if (first_tile > tiles_per_head) first_tile = tiles_per_head;
     }
@@ -269,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int n_tiles = g * tiles_h;
 
     // K_aug: row r = [1, 1, 1, 0, 0, 0, 0, 0] then an all-zero K half.
-    for (int i = threadIdx.x; i < C::kAugA / 16; i += kThreads) {
+    for (int i = threadIdx.x; i < C::kAugA / 16; i += C::kThreads) {
         uint4 v = make_uint4(0, 0, 0, 0);
         if (i < C::kBK) {
             const uint32_t one = 0x3F80u;  // bf16 1.0
@@ -290,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&s_full[s], 1);
-            mbar_init(&s_empty[s], 4);
+            mbar_init(&s_empty[s], 4 * C::kBlocks);
         }
         fence_barrier_init();
     }
@@ -302,8 +317,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (elect_one() && n_tiles > 0) {
-            mbar_arrive_expect_tx(bar_k, C::kKBytes);
-            for (int p = 0; p < C::kPanels; ++p) tma_load_3d(sK + p * (C::kBK * 128), &tk, bar_k, p * 64, k0, kslab);
+            mbar_arrive_expect_tx(bar_k, C::kBlocks * C::kKBytes);
+            for (int b = 0; b < C::kBlocks; ++b)
+                for (int p = 0; p < C::kPanels; ++p)
+                    tma_load_3d(sK + b * C::kKBytes + p * (C::kBK * 128), &tk, bar_k, p * 64, k0 + b * C::kBK, kslab);
             for (int j = 0; j < n_tiles; ++j) {
                 const int st = j % C::kStages;
                 const int hh = j / tiles_h, qt = first_tile + j % tiles_h;
@@ -326,18 +343,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             if (elect_one()) {
                 uint8_t* qs = sQ + st * C::kStageBytes;
-                const uint32_t d = tmem + sb * C::kBQ;
-#pragma unroll
-                for (int p = 0; p < C::kPanels; ++p) {
-                    const uint64_t a = desc_sw128(sK + p * (C::kBK * 128));
-                    const uint64_t b = desc_sw128(qs + p * (C::kBQ * 128));
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) mma_f16_ss(d, a + kk * 2, b + kk * 2, idesc, (p | kk) != 0);
-                }
-                // − λ_q: K_aug (ones, zero second K half via LBO) · Q_aug (−hi, −mid, −lo)
                 const uint64_t a_aug = desc_noswz(sAug, C::kBK * 16, 128);
                 const uint64_t b_aug = desc_noswz(qs + C::kQBytes, 0, 128);
-                mma_f16_ss(d, a_aug, b_aug, idesc, 1);
+#pragma unroll
+                for (int b = 0; b < C::kBlocks; ++b) {
+                    const uint32_t d = tmem + (sb * C::kBlocks + b) * C::kBQ;
+#pragma unroll
+                    for (int p = 0; p < C::kPanels; ++p) {
+                        const uint64_t a = desc_sw128(sK + b * C::kKBytes + p * (C::kBK * 128));
+                        const uint64_t bq = desc_sw128(qs + p * (C::kBQ * 128));
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) mma_f16_ss(d, a + kk * 2, bq + kk * 2, idesc, (p | kk) != 0);
+                    }
+                    // − λ_q: K_aug (ones; zero second K half via LBO) · Q_aug (−hi, −mid, −lo)
+                    mma_f16_ss(d, a_aug, b_aug, idesc, 1);
+                }
                 mma_commit(&s_full[sb]);
                 mma_commit(&q_empty[st]);
             }
@@ -345,51 +365,69 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= 4) {
         const uint32_t quad = warp & 3;
+        const int blk = (warp - 4) >> 2;
         const int r = quad * 32 + lane;
-        const int key = k0 + r;
+        const int key = k0 + blk * C::kBK + r;
         const int qmin = key - off;  // causal: queries >= qmin see this key
         float acc = kMax ? -INFINITY : 0.0f;
         for (int j = 0; j < n_tiles; ++j) {
             const int sb = j & 1;
             const int qbase = (first_tile + j % tiles_h) * C::kBQ;
-            int lo_col = causal ? qmin - qbase : 0;  // columns [lo_col, hi_col) valid
-            lo_col = lo_col < 0 ? 0 : lo_col;
-            const int hi_col = Nq - qbase < C::kBQ ? Nq - qbase : C::kBQ;
+            const int lo_col = causal ? max(qmin - qbase, 0) : 0;  // columns [lo_col, hi_col) valid
+            const int hi_col = min(Nq - qbase, C::kBQ);
             mbar_wait(&s_full[sb], (j >> 1) & 1);
             tc_fence_after();
-            const uint32_t base = tmem + ((quad * 32) << 16) + sb * C::kBQ;
-            // tcgen05.ld is warp-collective: skip a chunk only if masked for every
-            // lane (lane 0 holds the warp's smallest key, hence smallest lo_col).
-            const int lo_warp = __shfl_sync(0xffffffffu, lo_col, 0);
-#pragma unroll 1
-            for (int c0 = 0; c0 < C::kBQ; c0 += 32) {
-                if (c0 >= hi_col || c0 + 32 <= lo_warp) continue;
-                uint32_t rr[32];
-                tmem_ld32(base + c0, rr);
-                tmem_ld_wait();
-                const bool full = c0 >= lo_col && c0 + 32 <= hi_col;
-                if (kMax) {
-                    if (full) {
-#pragma unroll
-                        for (int u = 0; u < 32; u += 2) acc = max3f(acc, __uint_as_float(rr[u]), __uint_as_float(rr[u + 1]));
-                    } else {
-#pragma unroll
-                        for (int u = 0; u < 32; ++u)
-                            if (c0 + u >= lo_col && c0 + u < hi_col) acc = fmaxf(acc, __uint_as_float(rr[u]));
-                    }
-                } else {
-                    float s = 0.0f;
-#pragma unroll
-                    for (int u = 0; u < 32; ++u) {
-                        const float e = ex2(__uint_as_float(rr[u]) * c_log2);
-                        s += (full || (c0 + u >= lo_col && c0 + u < hi_col)) ? e : 0.0f;
-                    }
-                    acc += s;
-                }
-            }
+            const uint32_t base = tmem + ((quad * 32) << 16) + (sb * C::kBlocks + blk) * C::kBQ;
+            uint32_t r0[32], r1[32], r2[32], r3[32];
+            tmem_ld32(base, r0);
+            tmem_ld32(base + 32, r1);
+            tmem_ld32(base + 64, r2);
+            tmem_ld32(base + 96, r3);
+            tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[sb]);
+            float v[128];
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+                v[u] = __uint_as_float(r0[u]);
+                v[32 + u] = __uint_as_float(r1[u]);
+                v[64 + u] = __uint_as_float(r2[u]);
+                v[96 + u] = __uint_as_float(r3[u]);
+            }
+            const bool full = lo_col == 0 && hi_col == C::kBQ;
+            if (kMax) {
+                if (!full) {
+#pragma unroll
+                    for (int u = 0; u < 128; ++u) v[u] = (u >= lo_col && u < hi_col) ? v[u] : -INFINITY;
+                }
+                float m0 = acc, m1 = -INFINITY;
+#pragma unroll
+                for (int u = 0; u < 128; u += 4) {
+                    m0 = max3f(m0, v[u], v[u + 1]);
+                    m1 = max3f(m1, v[u + 2], v[u + 3]);
+                }
+                acc = fmaxf(m0, m1);
+            } else {
+                float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
+#pragma unroll
+                for (int u = 0; u < 128; u += 4) {
+                    const float e0 = ex2(v[u] * c_log2), e1 = ex2(v[u + 1] * c_log2);
+                    const float e2 = ex2(v[u + 2] * c_log2), e3 = ex2_poly(v[u + 3] * c_log2);
+                    if (full) {
+                        s0 += e0;
+                        s1 += e1;
+                        s2 += e2;
+                        s3 += e3;
+                    } else {
+                        s0 += (u >= lo_col && u < hi_col) ? e0 : 0.0f;
+                        s1 += (u + 1 >= lo_col && u + 1 < hi_col) ? e1 : 0.0f;
+                        s2 += (u + 2 >= lo_col && u + 2 < hi_col) ? e2 : 0.0f;
+                        s3 += (u + 3 >= lo_col && u + 3 < hi_col) ? e3 : 0.0f;
+                    }
+                }
+                acc += (s0 + s1) + (s2 + s3);
+            }
         }
         if (key < Nk) x_out[(int64_t)kslab * Nk + key] = kMax ? ex2(acc * c_log2) : acc;
     }
@@ -419,8 +457,8 @@ void run_lse(const ScoreShape& s, const void* q, const void* k, float* lse, __nv
     const CUtensorMap tk = make_tmap_3d(k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, s.Nk, s.L * s.Hkv, D * 2, D * 2 * s.Nk,
                                         64, C::kBK, 1, CU_TENSOR_MAP_SWIZZLE_128B);
     const dim3 grid((unsigned)((s.Nq + C::kBQ - 1) / C::kBQ), (unsigned)s.Hq, (unsigned)s.L);
-    score_lse_kernel<D><<<grid, kThreads, C::kSmem, st>>>(tq, tk, (int)s.Hq, (int)s.Hkv, (int)s.Nq, (int)s.Nk,
-                                                         s.causal ? 1 : 0, kLog2e / sqrtf((float)D), lse, lam);
+    score_lse_kernel<D><<<grid, C::kThreads, C::kSmem, st>>>(tq, tk, (int)s.Hq, (int)s.Hkv, (int)s.Nq, (int)s.Nk,
+                                                            s.causal ? 1 : 0, kLog2e / sqrtf((float)D), lse, lam);
     check_launch("score_lse_kernel");
 }
 
@@ -440,14 +478,15 @@ void run_pool(const ScoreShape& s, const void* q, const void* k, const __nv_bflo
                                         64, C::kBK, 1, CU_TENSOR_MAP_SWIZZLE_128B);
     const CUtensorMap tl = make_tmap_3d(lam, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 8, s.Nq, s.L * s.Hq, 16, 16 * s.Nq, 8,
                                         C::kBQ, 1, CU_TENSOR_MAP_SWIZZLE_NONE);
-    const dim3 grid((unsigned)((s.Nk + C::kBK - 1) / C::kBK), (unsigned)s.Hkv, (unsigned)s.L);
+    const int keys_per_cta = C::kBK * C::kBlocks;
+    const dim3 grid((unsigned)((s.Nk + keys_per_cta - 1) / keys_per_cta), (unsigned)s.Hkv, (unsigned)s.L);
     const float c = kLog2e / sqrtf((float)D);
     if (reduce_max) {
-        score_pool_kernel<D, true><<<grid, kThreads, C::kSmem, st>>>(tq, tk, tl, (int)s.Hq, (int)s.Hkv, (int)s.Nq,
-                                                                    (int)s.Nk, s.causal ? 1 : 0, c, x);
+        score_pool_kernel<D, true><<<grid, C::kThreads, C::kSmem, st>>>(tq, tk, tl, (int)s.Hq, (int)s.Hkv, (int)s.Nq,
+                                                                       (int)s.Nk, s.causal ? 1 : 0, c, x);
     } else {
-        score_pool_kernel<D, false><<<grid, kThreads, C::kSmem, st>>>(tq, tk, tl, (int)s.Hq, (int)s.Hkv, (int)s.Nq,
-                                                                     (int)s.Nk, s.causal ? 1 : 0, c, x);
+        score_pool_kernel<D, false><<<grid, C::kThreads, C::kSmem, st>>>(tq, tk, tl, (int)s.Hq, (int)s.Hkv,
+                                                                        (int)s.Nq, (int)s.Nk, s.causal ? 1 : 0, c, x);
     }
     check_launch("score_pool_kernel");
 }

@@ -86,3 +86,22 @@ def test_mapper_config_errors_mirror_reference():
         P.mapper_init_params(geo, P.MapperConfig(d_time=100, encoder_heads=8), 0)
     with pytest.raises(P.ConfigError):
         P.MapperConfig(stage_conv="sideways").as12()
+
+
+def _run_dropin():
+    import subprocess
+    exe = os.path.join(ROOT, "tests", "cpp", "test_dropin")
+    assert os.path.exists(exe), "build() compiles tests/cpp/test_dropin"
+    return subprocess.run([exe], capture_output=True, text=True, timeout=300)
+
+
+def test_cpp_dropin_header_host_logic():
+    """include/proxykv_b200/proxykv.hpp: reference signatures + exception taxonomy."""
+    r = _run_dropin()
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_header_on_gpu(gpu):
+    r = _run_dropin()
+    assert r.returncode == 0 and "gpu checks: ok" in r.stdout, r.stdout + r.stderr
