@@ -5,7 +5,7 @@
 // CTA = (256 queries = two 128-row tiles A/B, head, window); K/V tiles are
 // loaded once by TMA and shared by both query tiles.
 //   warp 0     TMA producer          warp 1   MMA issuer (one elected lane)
-//   warp 2     TMEM allocator        warps 4-7 / 8-11: softmax for tile A / B
+//   warp 0 also allocates TMEM;       warps 2-5 / 6-9: softmax for tile A / B
 // Per key tile j and query tile t:
 //   S_t = Q_t·K_jᵀ -> TMEM; softmax warps (one thread per row) load the row,
 //   compute P = 2^(c·s − m) with a lazily updated running max m (rescale O
@@ -28,7 +28,7 @@ constexpr int kTiles = 2;  // query tiles per CTA
 constexpr int kStages = 3;
 constexpr int kTileBytes = 128 * kD * 2;  // 16 KB: one Q, K or V tile
 constexpr int kPBytes = kBQ * kBK * 2;    // 32 KB: two 64-key swizzle panels
-constexpr int kThreads = 128 + 128 * kTiles;
+constexpr int kThreads = 64 + 128 * kTiles;  // 320 threads -> up to 204 registers per thread
 constexpr int kSmem = 1024 + kTileBytes * (kTiles + 2 * kStages) + kTiles * kPBytes + 256;
 constexpr uint32_t kTmemCols = 512;  // S_A, S_B (128 each) | O_A, O_B (64 each)
 constexpr uint32_t kColO = 256;
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
+    if (warp == 0) tmem_alloc(tmem_slot, kTmemCols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -141,8 +141,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (elect_one()) mma_commit(&kv_empty[j % kStages]);
             __syncwarp();
         }
-    } else if (warp >= 4) {
-        const int t = (warp - 4) >> 2;  // query tile
+    } else {
+        // softmax warps 2..9: tile = (warp - 2) / 4; TMEM lane quadrant = warp % 4
+        // (warps 2,3,4,5 cover quadrants 2,3,0,1 — all four rows blocks of the tile)
+        const int t = (int)(warp - 2) >> 2;
         const uint32_t quad = warp & 3;
         const uint32_t row = quad * 32 + lane;
         const uint32_t lane_addr = (quad * 32) << 16;
@@ -154,25 +156,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int valid = Lw - j * kBK;  // keys beyond are masked
             mbar_wait(&s_full[t], j & 1);
             tc_fence_after();
-            uint32_t r[4][32];
+            const bool tail = __any_sync(0xffffffffu, valid < kBK);  // warp-uniform: only the last key tile
+            // pass A: row max straight from TMEM (S stays there for pass B; keeps
+            // register pressure to 64 S values per thread)
+            float mt[8];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld32(s_addr + c * 32, r[c]);
-            tmem_ld_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s_empty[t]);
-            if (valid < kBK) {
+            for (int t8 = 0; t8 < 8; ++t8) mt[t8] = -INFINITY;
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
+            for (int c = 0; c < 4; c += 2) {
+                uint32_t r[2][32];
+                tmem_ld32(s_addr + c * 32, r[0]);
+                tmem_ld32(s_addr + (c + 1) * 32, r[1]);
+                tmem_ld_wait();
 #pragma unroll
-                    for (int u = 0; u < 32; ++u)
-                        if (c * 32 + u >= valid) r[c][u] = __float_as_uint(-INFINITY);
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    if (tail) {
+#pragma unroll
+                        for (int u = 0; u < 32; ++u)
+                            if ((c + h2) * 32 + u >= valid) r[h2][u] = __float_as_uint(-INFINITY);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 32; u += 16)
+#pragma unroll
+                        for (int t8 = 0; t8 < 8; ++t8)
+                            mt[t8] = max3f(mt[t8], __uint_as_float(r[h2][u + t8]), __uint_as_float(r[h2][u + t8 + 8]));
+                }
             }
-            float tmax = -INFINITY;
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-#pragma unroll
-                for (int u = 0; u < 32; u += 2) tmax = max3f(tmax, __uint_as_float(r[c][u]), __uint_as_float(r[c][u + 1]));
+            float tmax = max3f(max3f(mt[0], mt[1], mt[2]), max3f(mt[3], mt[4], mt[5]), fmaxf(mt[6], mt[7]));
             tmax *= scale_log2;
             // lazy rescale: warp-uniform decision (tcgen05.ld/st are warp-collective)
             const bool need = tmax > m + kRescale;
@@ -198,33 +208,55 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             // P = 2^(c·s − m) <= 2^8, rounded to fp16 and staged for P·V
             if (j > 0) mbar_wait(&o_done[t], (j - 1) & 1);  // P buffer free (PV(j-1) done)
-            float rs0 = 0.0f, rs1 = 0.0f;
+            // packed fp32x2 arguments/sums; 1 pair in 4 via the FMA-pipe polynomial
+            const uint64_t cc = pack2(scale_log2, scale_log2), nm = pack2(-m, -m);
+            uint64_t acc0 = pack2(0.0f, 0.0f), acc1 = acc0;
+            // pass B: re-read S in two 64-column halves
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint8_t* panel = pbuf + (c >> 1) * (kPBytes / 2);
+            for (int c2 = 0; c2 < 4; c2 += 2) {
+                uint32_t r[2][32];
+                tmem_ld32(s_addr + c2 * 32, r[0]);
+                tmem_ld32(s_addr + (c2 + 1) * 32, r[1]);
+                tmem_ld_wait();
+                if (tail) {
 #pragma unroll
-                for (int u = 0; u < 32; u += 8) {
-                    __align__(16) __half2 h[4];
+                    for (int h2 = 0; h2 < 2; ++h2)
 #pragma unroll
-                    for (int e = 0; e < 8; e += 2) {
-                        const float x0 = fmaf(__uint_as_float(r[c][u + e]), scale_log2, -m);
-                        const float x1 = fmaf(__uint_as_float(r[c][u + e + 1]), scale_log2, -m);
-                        const float p0 = ex2(x0);
-                        const float p1 = (e == 6) ? ex2_poly(x1) : ex2(x1);
-                        const __half2 hp = __floats2half2_rn(p0, p1);
-                        const float2 back = __half22float2(hp);
-                        rs0 += back.x;
-                        rs1 += back.y;
-                        h[e >> 1] = hp;
+                        for (int u = 0; u < 32; ++u)
+                            if ((c2 + h2) * 32 + u >= valid) r[h2][u] = __float_as_uint(-INFINITY);
+                }
+                uint8_t* panel = pbuf + (c2 >> 1) * (kPBytes / 2);
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+#pragma unroll
+                    for (int u = 0; u < 32; u += 8) {
+                        __align__(16) __half2 h[4];
+#pragma unroll
+                        for (int e = 0; e < 8; e += 2) {
+                            const uint64_t a = ffma2(
+                                pack2(__uint_as_float(r[h2][u + e]), __uint_as_float(r[h2][u + e + 1])), cc, nm);
+                            uint64_t pe;
+                            if (e == 6) {
+                                pe = ex2_poly2_d3(a);
+                            } else {
+                                const float2 x = unpack2(a);
+                                pe = pack2(ex2(x.x), ex2(x.y));
+                            }
+                            if (e & 2) acc1 = fadd2(acc1, pe);
+                            else acc0 = fadd2(acc0, pe);
+                            const float2 pf = unpack2(pe);
+                            h[e >> 1] = __floats2half2_rn(pf.x, pf.y);
+                        }
+                        *reinterpret_cast<uint4*>(panel + sw128_off(row, h2 * 32 + u)) = *reinterpret_cast<uint4*>(h);
                     }
-                    *reinterpret_cast<uint4*>(panel + sw128_off(row, ((c & 1) * 32) + u)) =
-                        *reinterpret_cast<uint4*>(h);
                 }
             }
-            l += rs0 + rs1;
+            const float2 rs = unpack2(fadd2(acc0, acc1));
+            l += rs.x + rs.y;
             tc_fence_before();
             fence_proxy_async_smem();
             __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[t]);  // S fully consumed (both passes)
             if (lane == 0) mbar_arrive(&p_full[t]);
         }
         mbar_wait(&o_done[t], (n_kv - 1) & 1);
@@ -256,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 2) {
+    if (warp == 0) {
         tc_fence_after();
         tmem_dealloc(tmem, kTmemCols);
     }

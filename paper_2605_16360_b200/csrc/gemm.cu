@@ -12,8 +12,12 @@ using namespace sm100;
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-B swizzle atom of fp16
-constexpr int kThreads = 256;
+constexpr int kEpiGroups = 2;  // epilogue warpgroups, each owning BN / kEpiGroups columns
+constexpr int kThreads = 128 + 128 * kEpiGroups;
 constexpr int kABytes = kBM * kBK * 2;
+// per epilogue warp: 32x32 fp32 staging tile (row stride 33: conflict-free)
+constexpr int kStageLd = 33;
+constexpr int kStageBufBytes = 4 * kEpiGroups * 32 * kStageLd * 4;
 
 __device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 
@@ -21,10 +25,10 @@ template <int BN, int NA, int NB>
 struct Cfg {
     static constexpr int kBBytes = BN * kBK * 2;
     static constexpr int kStageBytes = NA * kABytes + NB * kBBytes;
-    static constexpr int kBudget = 227 * 1024 - 2048;
+    static constexpr int kBudget = 227 * 1024 - 2048 - kStageBufBytes;
     static constexpr int kStagesRaw = kBudget / kStageBytes;
     static constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
-    static constexpr int kSmem = 1024 + kStages * kStageBytes + 256;
+    static constexpr int kSmem = 1024 + kStages * kStageBytes + 256 + kStageBufBytes;
     static constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
     static_assert(kStages >= 2, "not enough shared memory for 2 stages");
 };
@@ -98,6 +102,81 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpiParams& p, int64_t r
     }
 }
 
+// Warp-cooperative epilogue for a 32-row x 32-column accumulator chunk:
+// thread t holds row (row0 + t). The chunk is transposed through a padded smem
+// tile so global loads/stores are row-contiguous across the warp (128 B fp32
+// rows, or two 64 B fp16 rows per instruction) instead of 32 scattered
+// per-thread rows (partial-sector traffic).
+template <int EPI>
+__device__ __forceinline__ void epilogue_coalesced(const GemmEpiParams& p, int64_t row0, int64_t col0, int64_t M,
+                                                   int64_t N, const uint32_t (&r)[32], float* stg) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) stg[lane * kStageLd + j] = __uint_as_float(r[j]);
+    __syncwarp();
+    if (EPI == EPI_F16X || EPI == EPI_GELU_F16X) {
+        const int half = lane >> 4, cp = (lane & 15) * 2;
+        const int64_t col = col0 + cp;
+        const bool c0ok = col < N, c1ok = col + 1 < N;
+        const float b0 = (p.bias && c0ok) ? __ldg(p.bias + col) : 0.0f;
+        const float b1 = (p.bias && c1ok) ? __ldg(p.bias + col + 1) : 0.0f;
+#pragma unroll 4
+        for (int rr = 0; rr < 32; rr += 2) {
+            const int64_t row = row0 + rr + half;
+            if (row >= M) continue;
+            float x0 = stg[(rr + half) * kStageLd + cp] + b0;
+            float x1 = stg[(rr + half) * kStageLd + cp + 1] + b1;
+            if (EPI == EPI_GELU_F16X) {
+                x0 = gelu_erf(x0);
+                x1 = gelu_erf(x1);
+            }
+            const __half2 hi = __floats2half2_rn(x0, x1);
+            const float2 hb = __half22float2(hi);
+            const int64_t o = row * p.ldo + col;
+            if (c1ok) {
+                *reinterpret_cast<__half2*>(p.out_h + o) = hi;
+                if (p.out_l) *reinterpret_cast<__half2*>(p.out_l + o) = __floats2half2_rn(x0 - hb.x, x1 - hb.y);
+            } else if (c0ok) {
+                p.out_h[o] = __low2half(hi);
+                if (p.out_l) p.out_l[o] = __float2half_rn(x0 - hb.x);
+            }
+        }
+    } else {
+        const int64_t col = col0 + lane;
+        const bool cok = col < N;
+        const float b = (p.bias && cok) ? __ldg(p.bias + col) : 0.0f;
+        float* out = p.out_f32 + row0 * p.ldo + col;
+        // all global loads of the chunk are issued before any use (32 in flight per lane)
+        float extra[32];
+        if (EPI == EPI_RESID || (EPI == EPI_GELU_PE && p.pe)) {
+            int pr = 0;
+            if (EPI == EPI_GELU_PE) pr = (int)(row0 % p.lw);  // window position of row0; advanced with wrap below
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr) {
+                const bool ok = cok && row0 + rr < M;
+                if (EPI == EPI_RESID) {
+                    extra[rr] = ok ? out[rr * p.ldo] : 0.0f;
+                } else {
+                    extra[rr] = ok ? __ldg(p.pe + (int64_t)pr * p.ldo + col) : 0.0f;
+                    if (++pr == p.lw) pr = 0;
+                }
+            }
+        }
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) {
+            if (!cok || row0 + rr >= M) continue;
+            float x = stg[rr * kStageLd + lane] + b;
+            if (EPI == EPI_GELU_PE) {
+                x = gelu_erf(x);
+                if (p.pe) x += extra[rr];
+            }
+            if (EPI == EPI_RESID) x += extra[rr];
+            out[rr * p.ldo] = x;
+        }
+    }
+    __syncwarp();
+}
+
 template <int BN, int NA, int NB, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tA0, const __grid_constant__ CUtensorMap tA1,
@@ -111,6 +190,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull = empty + C::kStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* stagebuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tempty) + 256) +
+                      (warp_id() >= 4 ? (warp_id() - 4) * 32 * kStageLd : 0);
 
     const uint32_t warp = warp_id(), lane = lane_id();
     const int64_t tiles_m = (M + kBM - 1) / kBM, tiles_n = (N + BN - 1) / BN;
@@ -128,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);
+            mbar_init(&tempty[a], 4 * kEpiGroups);
         }
         fence_barrier_init();
     }
@@ -203,6 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= 4) {
         const uint32_t quad = warp & 3;
+        const int cg = (int)(warp - 4) >> 2;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
@@ -212,12 +294,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const int64_t row = m0 + quad * 32 + lane;
             const uint32_t taddr = tmem_base + ((quad * 32) << 16) + acc * BN;
+            // this warp's column group; the next chunk's TMEM load overlaps the
+            // current chunk's epilogue math (double-buffered registers)
+            const int cbeg = cg * (BN / kEpiGroups), cend = cbeg + BN / kEpiGroups;
+            uint32_t r[2][32];
+            tmem_ld32(taddr + cbeg, r[0]);
+            tmem_ld_wait();
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
-                uint32_t r[32];
-                tmem_ld32(taddr + c0, r);
+            for (int c0 = cbeg; c0 < cend; c0 += 64) {
+                if (c0 + 32 < cend) tmem_ld32(taddr + c0 + 32, r[1]);
+                if (n0 + c0 < N) epilogue_coalesced<EPI>(p, row - lane, n0 + c0, M, N, r[0], stagebuf);
                 tmem_ld_wait();
-                if (row < M && n0 + c0 < N) epilogue_chunk<EPI>(p, row, n0 + c0, N, r);
+                if (c0 + 32 < cend) {
+                    if (c0 + 64 < cend) tmem_ld32(taddr + c0 + 64, r[0]);
+                    if (n0 + c0 + 32 < N) epilogue_coalesced<EPI>(p, row - lane, n0 + c0 + 32, M, N, r[1], stagebuf);
+                    tmem_ld_wait();
+                }
             }
             tc_fence_before();
             __syncwarp();
@@ -271,6 +363,222 @@ void dispatch_planes(const GemmArgs& g, int sm, cudaStream_t st) {
     throw Error{PKV_ECONFIG, cat("unsupported GEMM plane combination na=", g.na, " nb=", g.nb)};
 }
 
+// ------------------------------------------------------------ CTA pair ----
+// cta_group::2 variant: a cluster of 2 CTAs computes a 256x256 tile. CTA r
+// loads A rows [m0 + 128r, +128) and B rows [n0 + 128r, +128) (half of each
+// operand per SM); the leader issues tcgen05.mma.cta_group::2 (M = 256), each
+// CTA's TMEM receives its 128 accumulator rows x 256 columns. Per-SM operand
+// traffic drops by a third vs the 128x256 single-CTA tile, which lets the
+// 4-plane FP16X3 stages fit 3-deep.
+template <int NA, int NB>
+struct Cfg2 {
+    static constexpr int kHalf = 128 * kBK * 2;  // 16 KB: one operand half-tile plane
+    static constexpr int kStageBytes = (NA + NB) * kHalf;
+    static constexpr int kBudget = 227 * 1024 - 2048 - kStageBufBytes;
+    static constexpr int kStagesRaw = kBudget / kStageBytes;
+    static constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
+    static constexpr int kSmem = 1024 + kStages * kStageBytes + 256 + kStageBufBytes;
+};
+
+template <int NA, int NB, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap tA0, const __grid_constant__ CUtensorMap tA1,
+                 const __grid_constant__ CUtensorMap tB0, const __grid_constant__ CUtensorMap tB1, GemmEpiParams p,
+                 int64_t M, int64_t N, int64_t K) {
+    using C = Cfg2<NA, NB>;
+    constexpr int BN = 256;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+    uint64_t* empty = full + C::kStages;
+    uint64_t* tfull = empty + C::kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* stagebuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tempty) + 256) +
+                      (warp_id() >= 4 ? (warp_id() - 4) * 32 * kStageLd : 0);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int64_t tiles_m = (M + 255) / 256, tiles_n = (N + BN - 1) / BN;
+    const int64_t tiles = tiles_m * tiles_n;
+    const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+    const int num_kb = (int)((K + kBK - 1) / kBK);
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tA0);
+        tma_prefetch(&tB0);
+        if (NA > 1) tma_prefetch(&tA1);
+        if (NB > 1) tma_prefetch(&tB1);
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(&full[s], 1);   // leader: arrive.expect_tx(both halves); bytes of both CTAs land here
+            mbar_init(&empty[s], 1);  // multicast commit from the leader's MMA
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 8 * kEpiGroups);  // epilogue warps of both CTAs (leader's copy is used)
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc_2sm(tmem_slot, 512);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t t = cluster; t < tiles; t += nclusters) {
+                const int32_t m0 = (int32_t)((t / tiles_n) * 256 + rank * 128);
+                const int32_t n0 = (int32_t)((t % tiles_n) * BN + rank * 128);
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* st = smem + stage * C::kStageBytes;
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
+                    tma_load_2d_2sm(st, &tA0, &full[stage], kb * kBK, m0);
+                    if (NA > 1) tma_load_2d_2sm(st + C::kHalf, &tA1, &full[stage], kb * kBK, m0);
+                    tma_load_2d_2sm(st + NA * C::kHalf, &tB0, &full[stage], kb * kBK, n0);
+                    if (NB > 1) tma_load_2d_2sm(st + (NA + 1) * C::kHalf, &tB1, &full[stage], kb * kBK, n0);
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader) {
+            constexpr uint32_t idesc = idesc_f16(256, BN, 0);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t t = cluster; t < tiles; t += nclusters) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + acc * BN;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        uint8_t* st = smem + stage * C::kStageBytes;
+                        const uint64_t a0 = desc_sw128(st);
+                        const uint64_t a1 = desc_sw128(st + C::kHalf);
+                        const uint64_t b0 = desc_sw128(st + NA * C::kHalf);
+                        const uint64_t b1 = desc_sw128(st + (NA + 1) * C::kHalf);
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 16; ++kk) {
+                            const uint64_t off = (uint64_t)(kk * 2);
+                            mma_f16_ss_2sm(d, a0 + off, b0 + off, idesc, (kb | kk) != 0);
+                            if (NA > 1) mma_f16_ss_2sm(d, a1 + off, b0 + off, idesc, 1);
+                            if (NB > 1) mma_f16_ss_2sm(d, a0 + off, b1 + off, idesc, 1);
+                        }
+                        mma_commit_2sm(&empty[stage], 0x3);
+                    }
+                    __syncwarp();
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                if (elect_one()) mma_commit_2sm(&tfull[acc], 0x3);
+                __syncwarp();
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        const uint32_t quad = warp & 3;
+        const int cg = (int)(warp - 4) >> 2;
+        const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t t = cluster; t < tiles; t += nclusters) {
+            const int64_t m0 = (t / tiles_n) * 256 + rank * 128;
+            const int64_t n0 = (t % tiles_n) * BN;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int64_t row = m0 + quad * 32 + lane;
+            const uint32_t taddr = tmem_base + ((quad * 32) << 16) + acc * BN;
+            // this warp's column group; the next chunk's TMEM load overlaps the
+            // current chunk's epilogue math (double-buffered registers)
+            const int cbeg = cg * (BN / kEpiGroups), cend = cbeg + BN / kEpiGroups;
+            uint32_t r[2][32];
+            tmem_ld32(taddr + cbeg, r[0]);
+            tmem_ld_wait();
+#pragma unroll 1
+            for (int c0 = cbeg; c0 < cend; c0 += 64) {
+                if (c0 + 32 < cend) tmem_ld32(taddr + c0 + 32, r[1]);
+                if (n0 + c0 < N) epilogue_coalesced<EPI>(p, row - lane, n0 + c0, M, N, r[0], stagebuf);
+                tmem_ld_wait();
+                if (c0 + 32 < cend) {
+                    if (c0 + 64 < cend) tmem_ld32(taddr + c0 + 64, r[0]);
+                    if (n0 + c0 + 32 < N) epilogue_coalesced<EPI>(p, row - lane, n0 + c0 + 32, M, N, r[1], stagebuf);
+                    tmem_ld_wait();
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc_2sm(tmem_base, 512);
+    }
+}
+
+template <int NA, int NB, int EPI>
+void launch2(const GemmArgs& g, int sm_count, cudaStream_t st) {
+    using C = Cfg2<NA, NB>;
+    auto kern = gemm2_kernel<NA, NB, EPI>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        PKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+        attr_set = true;
+    }
+    // B re-encoded with 128-row boxes (each CTA of the pair loads half of the N tile)
+    CUtensorMap b[2];
+    for (int q = 0; q < NB; ++q) {
+        b[q] = make_tmap_2d(g.b_ptr[q], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, (uint64_t)g.K, (uint64_t)g.N,
+                            (uint64_t)g.ldb * 2, kBK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    }
+    if (NB == 1) b[1] = b[0];
+    const int64_t tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256);
+    int64_t clusters = tiles < sm_count / 2 ? tiles : sm_count / 2;
+    kern<<<(unsigned)(2 * clusters), kThreads, C::kSmem, st>>>(g.a[0], g.a[1], b[0], b[1], g.p, g.M, g.N, g.K);
+    check_launch("gemm2_kernel");
+}
+
+template <int NA, int NB>
+void dispatch2_epi(const GemmArgs& g, int sm, cudaStream_t st) {
+    switch (g.epi) {
+        case EPI_F32: return launch2<NA, NB, EPI_F32>(g, sm, st);
+        case EPI_F16X: return launch2<NA, NB, EPI_F16X>(g, sm, st);
+        case EPI_GELU_F16X: return launch2<NA, NB, EPI_GELU_F16X>(g, sm, st);
+        case EPI_RESID: return launch2<NA, NB, EPI_RESID>(g, sm, st);
+        case EPI_GELU_PE: return launch2<NA, NB, EPI_GELU_PE>(g, sm, st);
+    }
+}
+
+void dispatch2(const GemmArgs& g, int sm, cudaStream_t st) {
+    if (g.na == 1 && g.nb == 1) return dispatch2_epi<1, 1>(g, sm, st);
+    if (g.na == 2 && g.nb == 1) return dispatch2_epi<2, 1>(g, sm, st);
+    if (g.na == 1 && g.nb == 2) return dispatch2_epi<1, 2>(g, sm, st);
+    if (g.na == 2 && g.nb == 2) return dispatch2_epi<2, 2>(g, sm, st);
+    throw Error{PKV_ECONFIG, cat("unsupported GEMM plane combination na=", g.na, " nb=", g.nb)};
+}
+
 }  // namespace
 
 void gemm_set_a(GemmArgs& g, int plane, const __half* a, int64_t M, int64_t K, int64_t lda) {
@@ -287,13 +595,13 @@ void gemm_set_b(GemmArgs& g, int plane, const __half* b, int64_t N, int64_t K, i
                               (uint32_t)g.bn, CU_TENSOR_MAP_SWIZZLE_128B);
     if (plane == 1) g.nb = 2;
     g.N = N;
+    g.b_ptr[plane] = b;
+    g.ldb = ldb;
 }
 
 void gemm_run(const GemmArgs& g, int sm_count, cudaStream_t st) {
     if (g.M == 0 || g.N == 0) return;
-    if (g.na == 1) {
-        // the plane-1 map is never dereferenced; pass plane 0 to keep the params valid
-    }
+    if (g.pair) return dispatch2(g, sm_count, st);
     switch (g.bn) {
         case 256: return dispatch_planes<256>(g, sm_count, st);
         case 128: return dispatch_planes<128>(g, sm_count, st);

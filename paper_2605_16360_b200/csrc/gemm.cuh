@@ -45,6 +45,10 @@ struct GemmArgs {
     int bn = 256;
     GemmEpi epi = EPI_F32;
     GemmEpiParams p;
+    // raw operands (the 2-CTA path re-encodes B with 128-row boxes)
+    const __half* b_ptr[2] = {nullptr, nullptr};
+    int64_t ldb = 0;
+    bool pair = false;  // use the CTA-pair (cta_group::2, 256x256 tile) kernel
 };
 
 // Builds the TMA maps for fp16 K-major planes: A rows of length K (row stride

@@ -445,6 +445,7 @@ void Mapper::gemm(const __half* a_h, const __half* a_l, int64_t M, const WeightP
                   GemmEpi epi, GemmEpiParams p, cudaStream_t st) {
     GemmArgs g;
     g.bn = pick_bn(w.N);
+    g.pair = use_pair && w.N >= 256 && M >= 256;  // cta_group::2 256x256 tiles for the big projections
     g.epi = epi;
     gemm_set_a(g, 0, a_h, M, w.K, w.K);
     g.a[1] = g.a[0];

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_fp16.h>
 
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <utility>
@@ -59,6 +60,7 @@ public:
     Config cfg;
     int na = 2, nb = 1;
     int64_t rows_cap = int64_t(1) << 20;  // rows per chunk (bounds the workspace)
+    bool use_pair = getenv("PKV_NO_PAIR") == nullptr;  // CTA-pair GEMMs (tuning/AB switch)
 
 private:
     WeightPlanes upload_planes(const std::vector<double>& W, int64_t N, int64_t K);

@@ -17,6 +17,8 @@
 // GQA: pass 2 walks the queries of all heads of a KV head's group.
 //
 // q bf16 [L, Hq, Nq, d], k bf16 [L, Hkv, Nk, d]; d ∈ {64, 128}.
+#include <cstdlib>
+
 #include "score.cuh"
 #include "sm100.cuh"
 
@@ -81,7 +83,7 @@ __device__ __forceinline__ void write_lam(__nv_bfloat16* dst, float lam) {
 }
 
 // ---------------------------------------------------------------- pass 1 --
-template <int D>
+template <int D, int kPolyPairs>
 __global__ void __launch_bounds__(P1<D>::kThreads, 1)
     score_lse_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk, int Hq, int Hkv,
                      int Nq, int Nk, int causal, float c_log2, float* __restrict__ lse_out,
@@ -193,24 +195,43 @@ __global__ void __launch_bounds__(P1<D>::kThreads, 1)
                 v[u] = __uint_as_float(ra[u]);
                 v[32 + u] = __uint_as_float(rb[u]);
             }
-            if (valid < 64) {
+            if (__any_sync(0xffffffffu, valid < 64)) {  // warp-uniform: only tail / diagonal tiles
 #pragma unroll
                 for (int u = 0; u < 64; ++u) v[u] = (u < valid) ? v[u] : -INFINITY;
             }
-            float cm = -INFINITY;
+            // max as a tree (8 independent FMNMX3 chains) to keep the dependency short
+            float mt[8];
 #pragma unroll
-            for (int u = 0; u < 64; u += 2) cm = max3f(cm, v[u], v[u + 1]);
+            for (int t8 = 0; t8 < 8; ++t8) mt[t8] = fmaxf(v[t8], v[t8 + 8]);
+#pragma unroll
+            for (int u = 16; u < 64; u += 16)
+#pragma unroll
+                for (int t8 = 0; t8 < 8; ++t8) mt[t8] = max3f(mt[t8], v[u + t8], v[u + t8 + 8]);
+            const float cm = max3f(max3f(mt[0], mt[1], mt[2]), max3f(mt[3], mt[4], mt[5]), fmaxf(mt[6], mt[7]));
             const float mn = fmaxf(m, cm * c_log2);
             if (mn == -INFINITY) continue;
-            float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
+            // packed fp32x2: FFMA2 for the arguments, FADD2 for the sums; of every
+            // 8 pairs, kPolyPairs go through the FMA-pipe polynomial, the rest MUFU
+            const uint64_t cc = pack2(c_log2, c_log2), nm = pack2(-mn, -mn);
+            uint64_t acc0 = pack2(0.0f, 0.0f), acc1 = acc0;
 #pragma unroll
-            for (int u = 0; u < 64; u += 4) {
-                s0 += ex2(fmaf(v[u], c_log2, -mn));
-                s1 += ex2(fmaf(v[u + 1], c_log2, -mn));
-                s2 += ex2(fmaf(v[u + 2], c_log2, -mn));
-                s3 += ex2_poly(fmaf(v[u + 3], c_log2, -mn));
+            for (int u = 0; u < 64; u += 16) {
+#pragma unroll
+                for (int pr = 0; pr < 8; ++pr) {
+                    const uint64_t a = ffma2(pack2(v[u + 2 * pr], v[u + 2 * pr + 1]), cc, nm);
+                    uint64_t e;
+                    if ((pr * kPolyPairs) % 8 + kPolyPairs >= 8 || (kPolyPairs == 8)) {
+                        e = ex2_poly2_d3(a);
+                    } else {
+                        const float2 x = unpack2(a);
+                        e = pack2(ex2(x.x), ex2(x.y));
+                    }
+                    if (pr & 1) acc1 = fadd2(acc1, e);
+                    else acc0 = fadd2(acc0, e);
+                }
             }
-            lsum = lsum * ex2(m - mn) + ((s0 + s1) + (s2 + s3));
+            const float2 ssum = unpack2(fadd2(acc0, acc1));
+            lsum = lsum * ex2(m - mn) + (ssum.x + ssum.y);
             m = mn;
         }
         part[seg * C::kBQ + r] = make_float2(m, lsum);
@@ -401,13 +422,15 @@ __global__ void __launch_bounds__(P2<D>::kThreads, 1)
 #pragma unroll
                     for (int u = 0; u < 128; ++u) v[u] = (u >= lo_col && u < hi_col) ? v[u] : -INFINITY;
                 }
-                float m0 = acc, m1 = -INFINITY;
+                float mt[8];
 #pragma unroll
-                for (int u = 0; u < 128; u += 4) {
-                    m0 = max3f(m0, v[u], v[u + 1]);
-                    m1 = max3f(m1, v[u + 2], v[u + 3]);
-                }
-                acc = fmaxf(m0, m1);
+                for (int t8 = 0; t8 < 8; ++t8) mt[t8] = fmaxf(v[t8], v[t8 + 8]);
+#pragma unroll
+                for (int u = 16; u < 128; u += 16)
+#pragma unroll
+                    for (int t8 = 0; t8 < 8; ++t8) mt[t8] = max3f(mt[t8], v[u + t8], v[u + t8 + 8]);
+                acc = max3f(acc, max3f(mt[0], mt[1], mt[2]),
+                            max3f(max3f(mt[3], mt[4], mt[5]), mt[6], mt[7]));
             } else {
                 float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
 #pragma unroll
@@ -448,8 +471,12 @@ template <int D>
 void run_lse(const ScoreShape& s, const void* q, const void* k, float* lse, __nv_bfloat16* lam, cudaStream_t st) {
     using C = P1<D>;
     static bool once = false;
+    static int poly = 3;
     if (!once) {
-        set_smem(score_lse_kernel<D>, C::kSmem);
+        set_smem(score_lse_kernel<D, 2>, C::kSmem);
+        set_smem(score_lse_kernel<D, 3>, C::kSmem);
+        set_smem(score_lse_kernel<D, 4>, C::kSmem);
+        if (const char* e = getenv("PKV_POLY_PAIRS")) poly = atoi(e);  // tuning knob: 2..4 of 8 pairs
         once = true;
     }
     const CUtensorMap tq = make_tmap_3d(q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, s.Nq, s.L * s.Hq, D * 2, D * 2 * s.Nq,
@@ -457,8 +484,9 @@ void run_lse(const ScoreShape& s, const void* q, const void* k, float* lse, __nv
     const CUtensorMap tk = make_tmap_3d(k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, s.Nk, s.L * s.Hkv, D * 2, D * 2 * s.Nk,
                                         64, C::kBK, 1, CU_TENSOR_MAP_SWIZZLE_128B);
     const dim3 grid((unsigned)((s.Nq + C::kBQ - 1) / C::kBQ), (unsigned)s.Hq, (unsigned)s.L);
-    score_lse_kernel<D><<<grid, C::kThreads, C::kSmem, st>>>(tq, tk, (int)s.Hq, (int)s.Hkv, (int)s.Nq, (int)s.Nk,
-                                                            s.causal ? 1 : 0, kLog2e / sqrtf((float)D), lse, lam);
+    auto kern = poly == 2 ? score_lse_kernel<D, 2> : (poly == 4 ? score_lse_kernel<D, 4> : score_lse_kernel<D, 3>);
+    kern<<<grid, C::kThreads, C::kSmem, st>>>(tq, tk, (int)s.Hq, (int)s.Hkv, (int)s.Nq, (int)s.Nk, s.causal ? 1 : 0,
+                                              kLog2e / sqrtf((float)D), lse, lam);
     check_launch("score_lse_kernel");
 }
 

@@ -87,6 +87,62 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// ----------------------------------------------------- clusters (CTA pairs)
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Address of the same smem object in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// 2-SM TMA: both CTAs of the pair load their half; the bytes complete on the
+// leader CTA's barrier (peer bit 24 of the shared::cluster address cleared).
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                                int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_2sm(uint32_t* smem_dst, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_2sm(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+// Pair MMA, issued by the leader CTA: D (M = 256 across both CTAs' TMEM) += A·Bᵀ.
+__device__ __forceinline__ void mma_f16_ss_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Commit the pair's MMAs to the same-offset barrier in every CTA of `mask`.
+__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+
 // ----------------------------------------------------------------- tcgen05
 // TMEM allocation: one full warp executes alloc/dealloc.
 __device__ __forceinline__ void tmem_alloc(uint32_t* smem_dst, uint32_t ncols) {
@@ -155,6 +211,73 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
 }
 
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 — two lanes' worth of
+// fp32 work per instruction slot).
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float2 unpack2(uint64_t v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+// Two 2^x (x <= 0) on the FMA pipe with packed FADD2/FFMA2 (see ex2_poly).
+__device__ __forceinline__ uint64_t ex2_poly2(uint64_t x2) {
+    float2 x = unpack2(x2);
+    x.x = fmaxf(x.x, -125.0f);
+    x.y = fmaxf(x.y, -125.0f);
+    const uint64_t xv = pack2(x.x, x.y);
+    const uint64_t t = fadd2(xv, pack2(12582912.0f, 12582912.0f));
+    const uint64_t j = fsub2(t, pack2(12582912.0f, 12582912.0f));
+    const uint64_t f = fsub2(xv, j);
+    uint64_t p = ffma2(pack2(0.009560510516166687f, 0.009560510516166687f), f,
+                       pack2(0.05591703951358795f, 0.05591703951358795f));
+    p = ffma2(p, f, pack2(0.24024981260299683f, 0.24024981260299683f));
+    p = ffma2(p, f, pack2(0.6931219696998596f, 0.6931219696998596f));
+    p = ffma2(p, f, pack2(0.9999991655349731f, 0.9999991655349731f));
+    const float2 pf = unpack2(p), tf = unpack2(t);
+    return pack2(__int_as_float(__float_as_int(tf.x) * 8388608 + __float_as_int(pf.x)),
+                 __int_as_float(__float_as_int(tf.y) * 8388608 + __float_as_int(pf.y)));
+}
+
+// Cheaper pair variant for sums that tolerate 8e-5 relative error per term
+// (the LSE pass): degree-3 fit of 2^f on [-0.5, 0.5] (max rel err 7.7e-5), and
+// the exponent insertion as shift+add (LEA on the ALU pipe, off the FMA pipe).
+__device__ __forceinline__ uint64_t ex2_poly2_d3(uint64_t x2) {
+    float2 x = unpack2(x2);
+    x.x = fmaxf(x.x, -125.0f);
+    x.y = fmaxf(x.y, -125.0f);
+    const uint64_t xv = pack2(x.x, x.y);
+    const uint64_t t = fadd2(xv, pack2(12582912.0f, 12582912.0f));
+    const uint64_t j = fsub2(t, pack2(12582912.0f, 12582912.0f));
+    const uint64_t f = fsub2(xv, j);
+    uint64_t p = ffma2(pack2(0.05508868396282196f, 0.05508868396282196f), f,
+                       pack2(0.24260404706001282f, 0.24260404706001282f));
+    p = ffma2(p, f, pack2(0.6932762265205383f, 0.6932762265205383f));
+    p = ffma2(p, f, pack2(0.9999289512634277f, 0.9999289512634277f));
+    const float2 pf = unpack2(p), tf = unpack2(t);
+    return pack2(__int_as_float((__float_as_int(tf.x) << 23) + __float_as_int(pf.x)),
+                 __int_as_float((__float_as_int(tf.y) << 23) + __float_as_int(pf.y)));
+}
 
 // 2^x for x <= 0 on the FMA pipe (FA4-style MUFU offload): x = j + f with
 // j = rint(x), f ∈ [-0.5, 0.5]; 2^f by a degree-4 fit (max rel err 2.7e-6);

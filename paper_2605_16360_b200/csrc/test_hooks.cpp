@@ -21,7 +21,8 @@ extern "C" pkv_status pkv_test_gemm(pkv_ctx ctx, const float* a_dev, int64_t M, 
         launch_split_f16(a_dev, (int64_t)a_el, ah, na > 1 ? al : nullptr, st);
         launch_split_f16(b_dev, (int64_t)b_el, bh, nb > 1 ? bl : nullptr, st);
         GemmArgs g;
-        g.bn = bn;
+        g.bn = bn == 512 ? 256 : bn;  // 512 selects the CTA-pair 256x256 kernel
+        g.pair = bn == 512;
         g.epi = static_cast<GemmEpi>(epi);
         gemm_set_a(g, 0, ah, M, K, K);
         g.a[1] = g.a[0];

@@ -104,3 +104,26 @@ def test_encoder_attention(gpu, nwin, Lw, heads):
     want = (a @ v).permute(0, 2, 1, 3).reshape(nwin * Lw, D)
     err = (out.double() - want).abs().max().item()
     assert err < 3e-3 * want.abs().max().item(), err
+
+
+@pytest.mark.parametrize("M,K,N,na,nb,epi", [(512, 512, 512, 2, 2, 0), (1000, 768, 512, 2, 2, 4), (2048, 512, 1536, 2, 2, 1),
+                                           (777, 512, 2048, 2, 2, 2), (640, 2048, 512, 2, 2, 3), (256, 64, 256, 1, 1, 0),
+                                           (300, 512, 700, 2, 1, 0)])
+def test_gemm_cta_pair(gpu, M, K, N, na, nb, epi):
+    """cta_group::2 (256x256 tile over a CTA pair) == plain fp64 reference."""
+    import torch
+    import paper_2605_16360_b200 as P
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    a = torch.randn(M, K, device="cuda", generator=g)
+    b = torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)
+    bias = torch.randn(N, device="cuda", generator=g)
+    pe = torch.randn(333, N, device="cuda", generator=g)
+    resid = torch.randn(M, N, device="cuda", generator=g)
+    out = resid.clone() if epi == 3 else torch.zeros(M, N, device="cuda")
+    P.check(_hooks()(gpu.h, a.data_ptr(), M, K, b.data_ptr(), N, na, nb, 512, epi, bias.data_ptr(), pe.data_ptr(), 333,
+                     out.data_ptr(), None))
+    x = _split_ref(a, na) @ _split_ref(b, nb).T + bias.double()
+    gelu = lambda t: 0.5 * t * (1 + torch.erf(t / math.sqrt(2)))
+    want = {0: x, 1: x, 2: gelu(x), 3: resid.double() + x, 4: gelu(x) + pe.double()[torch.arange(M, device="cuda") % 333]}[epi]
+    err = (out.double() - want).abs().max().item()
+    assert err <= 2e-5 * max(1.0, want.abs().max().item()), err
