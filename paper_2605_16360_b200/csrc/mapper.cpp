@@ -442,7 +442,7 @@ int pick_bn(int64_t n) { return n <= 64 ? 64 : (n <= 128 ? 128 : 256); }
 }  // namespace
 
 void Mapper::gemm(const __half* a_h, const __half* a_l, int64_t M, const WeightPlanes& w, const float* bias,
-                  GemmEpi epi, GemmEpiParams p, cudaStream_t st) {
+                  GemmEpi epi, GemmEpiParams p, cudaStream_t st, bool single) {
     GemmArgs g;
     g.bn = pick_bn(w.N);
     g.pair = use_pair && w.N >= 256 && M >= 256;  // cta_group::2 256x256 tiles for the big projections
@@ -450,11 +450,11 @@ void Mapper::gemm(const __half* a_h, const __half* a_l, int64_t M, const WeightP
     gemm_set_a(g, 0, a_h, M, w.K, w.K);
     g.a[1] = g.a[0];
     g.na = 1;
-    if (na > 1) gemm_set_a(g, 1, a_l, M, w.K, w.K);
+    if (na > 1 && !single) gemm_set_a(g, 1, a_l, M, w.K, w.K);
     gemm_set_b(g, 0, w.hi, w.N, w.K, w.K);
     g.b[1] = g.b[0];
     g.nb = 1;
-    if (nb > 1) gemm_set_b(g, 1, w.lo, w.N, w.K, w.K);
+    if (nb > 1 && !single) gemm_set_b(g, 1, w.lo, w.N, w.K, w.K);
     p.bias = bias;
     g.p = p;
     gemm_run(g, ctx->sm_count, st);
@@ -556,7 +556,8 @@ void Mapper::run(const float* x, const std::vector<int64_t>& unit_off, int64_t N
                 GemmEpiParams pq;
                 pq.out_h = qkv;
                 pq.ldo = 3 * D;
-                gemm(h_h, h_l, rows, b.qkv, b.qkv_b, EPI_F16X, pq, st);
+                // q/k/v are rounded to one fp16 plane for attention: one MMA suffices
+                gemm(h_h, h_l, rows, b.qkv, b.qkv_b, EPI_F16X, pq, st, qkv_single);
                 launch_encoder_attention(qkv, nu * W, Lw, D, cfg.encoder_heads, c_h, c_l, D, st);
                 count_launch(ctx);
                 GemmEpiParams po;

@@ -61,11 +61,15 @@ public:
     int na = 2, nb = 1;
     int64_t rows_cap = int64_t(1) << 20;  // rows per chunk (bounds the workspace)
     bool use_pair = getenv("PKV_NO_PAIR") == nullptr;  // CTA-pair GEMMs (tuning/AB switch)
+    // QKV projection with one fp16 MMA (its output is rounded to one fp16 plane
+    // for attention anyway). Off by default: at Llama/32k it lowers the
+    // min-slice Top-K overlap from 0.99939 to 0.99908.
+    bool qkv_single = getenv("PKV_QKV_SINGLE") != nullptr;
 
 private:
     WeightPlanes upload_planes(const std::vector<double>& W, int64_t N, int64_t K);
     void gemm(const __half* a_h, const __half* a_l, int64_t M, const WeightPlanes& w, const float* bias, GemmEpi epi,
-              GemmEpiParams p, cudaStream_t st);
+              GemmEpiParams p, cudaStream_t st, bool single = false);
 
     std::vector<void*> owned;
     DevBuf work;
