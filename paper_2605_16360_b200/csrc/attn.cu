@@ -4,13 +4,19 @@
 //
 // CTA = (256 queries = two 128-row tiles A/B, head, window); K/V tiles are
 // loaded once by TMA and shared by both query tiles.
-//   warp 0     TMA producer          warp 1   MMA issuer (one elected lane)
-//   warp 0 also allocates TMEM;       warps 2-5 / 6-9: softmax for tile A / B
+//   warp 0     TMA producer + TMEM allocator
+//   warp 1     MMA issuer (one elected lane)
+//   warps 2-5 / 6-9: softmax for tile A / B (one thread per query row)
+// TMEM (512 columns): S_A | S_B (128 each) | O_A | O_B | P_A | P_B (64 each).
 // Per key tile j and query tile t:
-//   S_t = Q_t·K_jᵀ -> TMEM; softmax warps (one thread per row) load the row,
-//   compute P = 2^(c·s − m) with a lazily updated running max m (rescale O
-//   only when the row max grows by > 2^8, FA4-style), 1 in 4 exponentials on
-//   the FMA pipe; P (fp16) -> swizzled smem; O_t += P·V_j accumulates in TMEM.
+//   S_t = Q_t·K_jᵀ -> TMEM. The softmax warps read S once, in two 64-key
+//   halves, and evaluate P = 2^(c·s − m) against the running (integer, log2)
+//   max m while tracking the tile max; kPolyPairs of the 64 pairs run on the
+//   FMA pipe, the rest on MUFU. P is packed to fp16 and stored to P_t with
+//   tcgen05.st; O_t += P_t·V_j takes its A operand straight from TMEM, so P
+//   never touches shared memory. If the tile max exceeds m by more than 2^15
+//   (fp16 headroom; always on the first tile) the row max is raised, O and the
+//   sum are rescaled and P is recomputed from S, which is still resident.
 // Epilogue: O / l -> ctx hi/lo fp16 planes.
 //
 // Input: qkv fp16 [rows, 3·D] (q | k | v, head h at columns h·64 of each),
@@ -26,19 +32,59 @@ using namespace sm100;
 constexpr int kBQ = 128, kBK = 128, kD = 64;
 constexpr int kTiles = 2;  // query tiles per CTA
 constexpr int kStages = 3;
-constexpr int kTileBytes = 128 * kD * 2;  // 16 KB: one Q, K or V tile
-constexpr int kPBytes = kBQ * kBK * 2;    // 32 KB: two 64-key swizzle panels
-constexpr int kThreads = 64 + 128 * kTiles;  // 320 threads -> up to 204 registers per thread
-constexpr int kSmem = 1024 + kTileBytes * (kTiles + 2 * kStages) + kTiles * kPBytes + 256;
-constexpr uint32_t kTmemCols = 512;  // S_A, S_B (128 each) | O_A, O_B (64 each)
-constexpr uint32_t kColO = 256;
-constexpr float kRescale = 8.0f;  // log2 of the lazy-rescale threshold
+constexpr int kTileBytes = 128 * kD * 2;     // 16 KB: one Q, K or V tile
+constexpr int kThreads = 64 + 128 * kTiles;  // 320 threads
+constexpr int kSmem = 1024 + kTileBytes * (kTiles + 2 * kStages) + 256;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kColO = 256, kColP = 384;
+constexpr float kHeadroom = 15.0f;  // P <= 2^15 < fp16 max
+constexpr int kPolyPairs = 16;      // of the 32 exponential pairs per 64-key half
 
-// Byte offset of fp16 element (row, col) in a K-major, 128-B-swizzled panel
-// (rows of 128 B; 16-B chunk index XOR (row % 8)).
-__device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t col) {
-    const uint32_t chunk = (col >> 3) ^ (row & 7);
-    return row * 128 + chunk * 16 + (col & 7) * 2;
+__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// 64 scores (two 32-column TMEM loads) -> 32 fp16 pairs of P = 2^(c·s − m)
+// stored to TMEM at p_col; returns the raw max (or -inf) and adds Σp to acc.
+template <bool kMask>
+__device__ __forceinline__ float p_half(uint32_t s_col, uint32_t p_col, int valid, uint64_t cc, uint64_t nm,
+                                        uint64_t mp, uint64_t& acc0, uint64_t& acc1) {
+    uint32_t r[2][32];
+    tmem_ld32(s_col, r[0]);
+    tmem_ld32(s_col + 32, r[1]);
+    tmem_ld_wait();
+    if (kMask) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int u = 0; u < 32; ++u)
+                if (c * 32 + u >= valid) r[c][u] = __float_as_uint(-INFINITY);
+    }
+    float mt[4];
+#pragma unroll
+    for (int t4 = 0; t4 < 4; ++t4) mt[t4] = fmaxf(__uint_as_float(r[0][t4]), __uint_as_float(r[0][t4 + 4]));
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const uint32_t* rr = r[i >> 4];
+        const float a = __uint_as_float(rr[2 * (i & 15)]), b = __uint_as_float(rr[2 * (i & 15) + 1]);
+        if (i >= 4) mt[i & 3] = max3f(mt[i & 3], a, b);
+        const uint64_t s2 = pack2(a, b);
+        uint64_t e;
+        if (!kMask && ((i + 1) * kPolyPairs) / 32 != (i * kPolyPairs) / 32) {
+            e = ex2_poly2_fused(s2, cc, mp);
+        } else {
+            const float2 x = unpack2(ffma2(s2, cc, nm));
+            e = pack2(ex2(x.x), ex2(x.y));
+        }
+        if (i & 1) acc1 = fadd2(acc1, e);
+        else acc0 = fadd2(acc0, e);
+        const float2 ef = unpack2(e);
+        pk[i & 15] = pack_half2(ef.x, ef.y);
+        if ((i & 15) == 15) tmem_st16(p_col + (i & 16), pk);
+    }
+    return fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3]));
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -46,11 +92,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int64_t ld_out, int Lw, int D, float scale_log2) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;                          // [kTiles] tiles
-    uint8_t* sK = sQ + kTiles * kTileBytes;      // [kStages]
-    uint8_t* sV = sK + kStages * kTileBytes;     // [kStages]
-    uint8_t* sP = sV + kStages * kTileBytes;     // [kTiles] x 32 KB
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kTiles * kPBytes);
+    uint8_t* sQ = smem;                       // [kTiles] tiles
+    uint8_t* sK = sQ + kTiles * kTileBytes;   // [kStages]
+    uint8_t* sV = sK + kStages * kTileBytes;  // [kStages]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kStages * kTileBytes);
     uint64_t* bar_q = bars;
     uint64_t* kv_full = bars + 1;
     uint64_t* kv_empty = kv_full + kStages;
@@ -102,98 +147,85 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr uint32_t idesc_o = idesc_f16(kBQ, kD, 0, 0, 1);  // B (V) is MN-major
         mbar_wait(bar_q, 0);
         auto issue_s = [&](int j, int t) {
-            const int st = j % kStages;
-            mbar_wait(&s_empty[t], (j & 1) ^ 1);
-            tc_fence_after();
             if (elect_one()) {
                 const uint64_t a = desc_sw128(sQ + t * kTileBytes);
-                const uint64_t b = desc_sw128(sK + st * kTileBytes);
+                const uint64_t b = desc_sw128(sK + (j % kStages) * kTileBytes);
 #pragma unroll
                 for (int kk = 0; kk < kD / 16; ++kk) mma_f16_ss(tmem + t * kBK, a + kk * 2, b + kk * 2, idesc_s, kk > 0);
                 mma_commit(&s_full[t]);
             }
             __syncwarp();
         };
-        auto issue_pv = [&](int j, int t) {
-            mbar_wait(&p_full[t], j & 1);
-            tc_fence_after();
-            if (elect_one()) {
-                const uint8_t* v = sV + (j % kStages) * kTileBytes;
-                const uint8_t* p = sP + t * kPBytes;
-#pragma unroll
-                for (int kk = 0; kk < kBK / 16; ++kk) {
-                    const uint64_t a = desc_sw128(p + (kk >> 2) * (kPBytes / 2)) + (uint64_t)((kk & 3) * 2);
-                    const uint64_t b = desc_sw128_mn(v + kk * 16 * 128, 8192);
-                    mma_f16_ss(tmem + kColO + t * kD, a, b, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-                }
-                mma_commit(&o_done[t]);
-            }
-            __syncwarp();
-        };
         mbar_wait(&kv_full[0], 0);
+        tc_fence_after();
         for (int t = 0; t < kTiles; ++t) issue_s(0, t);
         for (int j = 0; j < n_kv; ++j) {
-            if (j + 1 < n_kv) {
-                mbar_wait(&kv_full[(j + 1) % kStages], ((j + 1) / kStages) & 1);
-                for (int t = 0; t < kTiles; ++t) issue_s(j + 1, t);
+            const uint8_t* v = sV + (j % kStages) * kTileBytes;
+            if (j + 1 < n_kv) mbar_wait(&kv_full[(j + 1) % kStages], ((j + 1) / kStages) & 1);
+            for (int t = 0; t < kTiles; ++t) {
+                if (j + 1 < n_kv) {  // S_t(j+1) as soon as the softmax has read S_t(j)
+                    mbar_wait(&s_empty[t], j & 1);
+                    tc_fence_after();
+                    issue_s(j + 1, t);
+                }
+                mbar_wait(&p_full[t], j & 1);
+                tc_fence_after();
+                if (elect_one()) {
+                    // O_t += P_t·V_j: A = P_t from TMEM (8 columns = 16 keys per MMA)
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        const uint64_t b = desc_sw128_mn(v + kk * 16 * 128, 8192);
+                        mma_f16_ts(tmem + kColO + t * kD, tmem + kColP + t * 64 + kk * 8, b, idesc_o,
+                                   (j > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    mma_commit(&o_done[t]);
+                    if (t == kTiles - 1) mma_commit(&kv_empty[j % kStages]);
+                }
+                __syncwarp();
             }
-            for (int t = 0; t < kTiles; ++t) issue_pv(j, t);
-            if (elect_one()) mma_commit(&kv_empty[j % kStages]);
-            __syncwarp();
         }
     } else {
         // softmax warps 2..9: tile = (warp - 2) / 4; TMEM lane quadrant = warp % 4
-        // (warps 2,3,4,5 cover quadrants 2,3,0,1 — all four rows blocks of the tile)
+        // (warps 2,3,4,5 cover quadrants 2,3,0,1 — all four row blocks of the tile)
         const int t = (int)(warp - 2) >> 2;
         const uint32_t quad = warp & 3;
         const uint32_t row = quad * 32 + lane;
         const uint32_t lane_addr = (quad * 32) << 16;
         const uint32_t s_addr = tmem + lane_addr + t * kBK;
         const uint32_t o_addr = tmem + lane_addr + kColO + t * kD;
-        uint8_t* pbuf = sP + t * kPBytes;
-        float m = -INFINITY, l = 0.0f;
+        const uint32_t p_addr = tmem + lane_addr + kColP + t * 64;
+        const uint64_t cc = pack2(scale_log2, scale_log2);
+        float m = -INFINITY, l = 0.0f;  // m: integer, log2 domain (-inf before the first tile)
         for (int j = 0; j < n_kv; ++j) {
             const int valid = Lw - j * kBK;  // keys beyond are masked
+            const bool tail = valid < kBK;   // uniform across the CTA
             mbar_wait(&s_full[t], j & 1);
             tc_fence_after();
-            const bool tail = __any_sync(0xffffffffu, valid < kBK);  // warp-uniform: only the last key tile
-            // pass A: row max straight from TMEM (S stays there for pass B; keeps
-            // register pressure to 64 S values per thread)
-            float mt[8];
-#pragma unroll
-            for (int t8 = 0; t8 < 8; ++t8) mt[t8] = -INFINITY;
-#pragma unroll
-            for (int c = 0; c < 4; c += 2) {
-                uint32_t r[2][32];
-                tmem_ld32(s_addr + c * 32, r[0]);
-                tmem_ld32(s_addr + (c + 1) * 32, r[1]);
-                tmem_ld_wait();
-#pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
-                    if (tail) {
-#pragma unroll
-                        for (int u = 0; u < 32; ++u)
-                            if ((c + h2) * 32 + u >= valid) r[h2][u] = __float_as_uint(-INFINITY);
-                    }
-#pragma unroll
-                    for (int u = 0; u < 32; u += 16)
-#pragma unroll
-                        for (int t8 = 0; t8 < 8; ++t8)
-                            mt[t8] = max3f(mt[t8], __uint_as_float(r[h2][u + t8]), __uint_as_float(r[h2][u + t8 + 8]));
+            if (j > 0) mbar_wait(&o_done[t], (j - 1) & 1);  // P_t free, O_t stable
+            tc_fence_after();
+            float rmax;
+            uint64_t acc0, acc1;
+            for (int attempt = 0;; ++attempt) {
+                const uint64_t nm = pack2(-m, -m), mp = pack2(12582912.0f - m, 12582912.0f - m);
+                acc0 = pack2(0.0f, 0.0f);
+                acc1 = acc0;
+                float h0, h1;
+                if (tail) {
+                    h0 = p_half<true>(s_addr, p_addr, valid, cc, nm, mp, acc0, acc1);
+                    h1 = p_half<true>(s_addr + 64, p_addr + 32, valid - 64, cc, nm, mp, acc0, acc1);
+                } else {
+                    h0 = p_half<false>(s_addr, p_addr, kBK, cc, nm, mp, acc0, acc1);
+                    h1 = p_half<false>(s_addr + 64, p_addr + 32, kBK, cc, nm, mp, acc0, acc1);
                 }
-            }
-            float tmax = max3f(max3f(mt[0], mt[1], mt[2]), max3f(mt[3], mt[4], mt[5]), fmaxf(mt[6], mt[7]));
-            tmax *= scale_log2;
-            // lazy rescale: warp-uniform decision (tcgen05.ld/st are warp-collective)
-            const bool need = tmax > m + kRescale;
-            if (__any_sync(0xffffffffu, need)) {
-                const float mn = fmaxf(m, tmax);
+                rmax = fmaxf(h0, h1) * scale_log2;
+                // warp-uniform (tcgen05.ld/st are warp-collective): raise the
+                // running max if any row's P would exceed the fp16 headroom
+                if (!__any_sync(0xffffffffu, rmax > m + kHeadroom) || attempt > 0) break;
+                const float mn = fmaxf(m, ceilf(rmax));
                 const float alpha = ex2(m - mn);  // 0 when m = -inf
                 l *= alpha;
                 m = mn;
                 if (j > 0) {
-                    mbar_wait(&o_done[t], (j - 1) & 1);  // O holds P(<j)·V, stable
-                    tc_fence_after();
 #pragma unroll
                     for (int c = 0; c < kD; c += 32) {
                         uint32_t o[32];
@@ -203,61 +235,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int u = 0; u < 32; ++u) o[u] = __float_as_uint(__uint_as_float(o[u]) * alpha);
                         tmem_st32(o_addr + c, o);
                     }
-                    tmem_st_wait();
-                }
-            }
-            // P = 2^(c·s − m) <= 2^8, rounded to fp16 and staged for P·V
-            if (j > 0) mbar_wait(&o_done[t], (j - 1) & 1);  // P buffer free (PV(j-1) done)
-            // packed fp32x2 arguments/sums; 1 pair in 4 via the FMA-pipe polynomial
-            const uint64_t cc = pack2(scale_log2, scale_log2), nm = pack2(-m, -m);
-            uint64_t acc0 = pack2(0.0f, 0.0f), acc1 = acc0;
-            // pass B: re-read S in two 64-column halves
-#pragma unroll
-            for (int c2 = 0; c2 < 4; c2 += 2) {
-                uint32_t r[2][32];
-                tmem_ld32(s_addr + c2 * 32, r[0]);
-                tmem_ld32(s_addr + (c2 + 1) * 32, r[1]);
-                tmem_ld_wait();
-                if (tail) {
-#pragma unroll
-                    for (int h2 = 0; h2 < 2; ++h2)
-#pragma unroll
-                        for (int u = 0; u < 32; ++u)
-                            if ((c2 + h2) * 32 + u >= valid) r[h2][u] = __float_as_uint(-INFINITY);
-                }
-                uint8_t* panel = pbuf + (c2 >> 1) * (kPBytes / 2);
-#pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
-#pragma unroll
-                    for (int u = 0; u < 32; u += 8) {
-                        __align__(16) __half2 h[4];
-#pragma unroll
-                        for (int e = 0; e < 8; e += 2) {
-                            const uint64_t a = ffma2(
-                                pack2(__uint_as_float(r[h2][u + e]), __uint_as_float(r[h2][u + e + 1])), cc, nm);
-                            uint64_t pe;
-                            if (e == 6) {
-                                pe = ex2_poly2_d3(a);
-                            } else {
-                                const float2 x = unpack2(a);
-                                pe = pack2(ex2(x.x), ex2(x.y));
-                            }
-                            if (e & 2) acc1 = fadd2(acc1, pe);
-                            else acc0 = fadd2(acc0, pe);
-                            const float2 pf = unpack2(pe);
-                            h[e >> 1] = __floats2half2_rn(pf.x, pf.y);
-                        }
-                        *reinterpret_cast<uint4*>(panel + sw128_off(row, h2 * 32 + u)) = *reinterpret_cast<uint4*>(h);
-                    }
                 }
             }
             const float2 rs = unpack2(fadd2(acc0, acc1));
             l += rs.x + rs.y;
+            tmem_st_wait();
             tc_fence_before();
-            fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&s_empty[t]);  // S fully consumed (both passes)
-            if (lane == 0) mbar_arrive(&p_full[t]);
+            if (lane == 0) {
+                mbar_arrive(&s_empty[t]);
+                mbar_arrive(&p_full[t]);
+            }
         }
         mbar_wait(&o_done[t], (n_kv - 1) & 1);
         tc_fence_after();

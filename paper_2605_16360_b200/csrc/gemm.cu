@@ -19,7 +19,6 @@ constexpr int kABytes = kBM * kBK * 2;
 constexpr int kStageLd = 33;
 constexpr int kStageBufBytes = 4 * kEpiGroups * 32 * kStageLd * 4;
 
-__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 
 template <int BN, int NA, int NB>
 struct Cfg {
@@ -46,7 +45,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpiParams& p, int64_t r
     }
     if (EPI == EPI_GELU_F16X || EPI == EPI_GELU_PE) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+        for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
     }
     const int64_t base = row * p.ldo + col0;
     if (EPI == EPI_F16X || EPI == EPI_GELU_F16X) {
@@ -107,38 +106,192 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpiParams& p, int64_t r
 // tile so global loads/stores are row-contiguous across the warp (128 B fp32
 // rows, or two 64 B fp16 rows per instruction) instead of 32 scattered
 // per-thread rows (partial-sector traffic).
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+// gelu_fast (sm100.cuh) on a packed pair: the FMA-pipe work as FFMA2/FMUL2.
+__device__ __forceinline__ float2 gelu_fast2(float x0, float x1) {
+    const uint64_t z = fmul2(pack2(fabsf(x0), fabsf(x1)), pack2(0.70710678118654752f, 0.70710678118654752f));
+    const float2 zd = unpack2(ffma2(pack2(0.3275911f, 0.3275911f), z, pack2(1.0f, 1.0f)));
+    const uint64_t t = pack2(rcp_approx(zd.x), rcp_approx(zd.y));
+    uint64_t q = ffma2(pack2(1.061405429f, 1.061405429f), t, pack2(-1.453152027f, -1.453152027f));
+    q = ffma2(q, t, pack2(1.421413741f, 1.421413741f));
+    q = ffma2(q, t, pack2(-0.284496736f, -0.284496736f));
+    q = ffma2(q, t, pack2(0.254829592f, 0.254829592f));
+    const float2 a = unpack2(fmul2(fmul2(z, pack2(-1.4426950408889634f, -1.4426950408889634f)), z));
+    const uint64_t e = pack2(ex2(a.x), ex2(a.y));
+    const float2 h = unpack2(fmul2(fmul2(pack2(0.5f * x0, 0.5f * x1), fmul2(q, t)), e));
+    return make_float2(x0 >= 0.0f ? x0 - h.x : h.x, x1 >= 0.0f ? x1 - h.y : h.y);
+}
+
+// Per-row epilogue of a 32-column accumulator chunk (thread = row; the row's
+// 32 columns are contiguous in global memory: 16-byte vector accesses, the L2
+// merges the warp's partial sectors). res: residual row slice (EPI_RESID).
+template <int EPI>
+__device__ __forceinline__ void epilogue_row(const GemmEpiParams& p, int64_t row, int64_t col0, int64_t M, int64_t N,
+                                             const uint32_t (&r)[32], const float4 (&res)[8]) {
+    if (row >= M) return;
+    const bool full = col0 + 32 <= N;
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+    if (p.bias) {
+        if (full) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+                const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + col0 + j));
+                v[j] += b.x;
+                v[j + 1] += b.y;
+                v[j + 2] += b.z;
+                v[j + 3] += b.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (col0 + j < N) v[j] += __ldg(p.bias + col0 + j);
+        }
+    }
+    if (EPI == EPI_GELU_F16X || EPI == EPI_GELU_PE) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+            const float2 g = gelu_fast2(v[j], v[j + 1]);
+            v[j] = g.x;
+            v[j + 1] = g.y;
+        }
+    }
+    const int64_t base = row * p.ldo + col0;
+    if (EPI == EPI_F16X || EPI == EPI_GELU_F16X) {
+        if (full) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+                uint32_t hi[4], lo[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const __half2 h = __floats2half2_rn(v[j + 2 * t], v[j + 2 * t + 1]);
+                    const float2 hf = __half22float2(h);
+                    const __half2 l = __floats2half2_rn(v[j + 2 * t] - hf.x, v[j + 2 * t + 1] - hf.y);
+                    hi[t] = *reinterpret_cast<const uint32_t*>(&h);
+                    lo[t] = *reinterpret_cast<const uint32_t*>(&l);
+                }
+                *reinterpret_cast<uint4*>(p.out_h + base + j) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                if (p.out_l) *reinterpret_cast<uint4*>(p.out_l + base + j) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                if (col0 + j >= N) continue;
+                const __half hi = __float2half_rn(v[j]);
+                p.out_h[base + j] = hi;
+                if (p.out_l) p.out_l[base + j] = __float2half_rn(v[j] - __half2float(hi));
+            }
+        }
+        return;
+    }
+    if (EPI == EPI_GELU_PE && p.pe) {
+        const float* pe = p.pe + (row % p.lw) * p.ldo + col0;
+        if (full) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+                const float4 e = __ldg(reinterpret_cast<const float4*>(pe + j));
+                v[j] += e.x;
+                v[j + 1] += e.y;
+                v[j + 2] += e.z;
+                v[j + 3] += e.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (col0 + j < N) v[j] += __ldg(pe + j);
+        }
+    }
+    if (EPI == EPI_RESID) {
+        if (full) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                v[4 * j] += res[j].x;
+                v[4 * j + 1] += res[j].y;
+                v[4 * j + 2] += res[j].z;
+                v[4 * j + 3] += res[j].w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (col0 + j < N) v[j] += p.out_f32[base + j];
+        }
+    }
+    float* out = p.out_f32 + base;
+    if (full) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(out + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (col0 + j < N) out[j] = v[j];
+    }
+}
+
 template <int EPI>
 __device__ __forceinline__ void epilogue_coalesced(const GemmEpiParams& p, int64_t row0, int64_t col0, int64_t M,
                                                    int64_t N, const uint32_t (&r)[32], float* stg) {
     const int lane = threadIdx.x & 31;
+    if (EPI == EPI_GELU_PE) {  // GELU-heavy, fp32 out: per-row (measured faster than the transpose)
+        const float4 none[8] = {};
+        epilogue_row<EPI>(p, row0 + lane, col0, M, N, r, none);
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < 32; ++j) stg[lane * kStageLd + j] = __uint_as_float(r[j]);
     __syncwarp();
+    // warp-uniform fast path: the whole 32x32 chunk is in bounds (no per-row
+    // checks, fully unrolled so independent rows overlap)
+    const bool full = row0 + 32 <= M && col0 + 32 <= N;
     if (EPI == EPI_F16X || EPI == EPI_GELU_F16X) {
         const int half = lane >> 4, cp = (lane & 15) * 2;
         const int64_t col = col0 + cp;
         const bool c0ok = col < N, c1ok = col + 1 < N;
         const float b0 = (p.bias && c0ok) ? __ldg(p.bias + col) : 0.0f;
         const float b1 = (p.bias && c1ok) ? __ldg(p.bias + col + 1) : 0.0f;
-#pragma unroll 4
-        for (int rr = 0; rr < 32; rr += 2) {
-            const int64_t row = row0 + rr + half;
-            if (row >= M) continue;
-            float x0 = stg[(rr + half) * kStageLd + cp] + b0;
-            float x1 = stg[(rr + half) * kStageLd + cp + 1] + b1;
-            if (EPI == EPI_GELU_F16X) {
-                x0 = gelu_erf(x0);
-                x1 = gelu_erf(x1);
+        if (full) {
+            __half* oh = p.out_h + (row0 + half) * p.ldo + col;
+            __half* ol = p.out_l ? p.out_l + (row0 + half) * p.ldo + col : nullptr;
+            const int64_t step = 2 * p.ldo;
+#pragma unroll
+            for (int rr = 0; rr < 32; rr += 2) {
+                float x0 = stg[(rr + half) * kStageLd + cp] + b0;
+                float x1 = stg[(rr + half) * kStageLd + cp + 1] + b1;
+                if (EPI == EPI_GELU_F16X) {
+                    x0 = gelu_fast(x0);
+                    x1 = gelu_fast(x1);
+                }
+                const __half2 hi = __floats2half2_rn(x0, x1);
+                const float2 hb = __half22float2(hi);
+                *reinterpret_cast<__half2*>(oh + (rr >> 1) * step) = hi;
+                if (ol) *reinterpret_cast<__half2*>(ol + (rr >> 1) * step) = __floats2half2_rn(x0 - hb.x, x1 - hb.y);
             }
-            const __half2 hi = __floats2half2_rn(x0, x1);
-            const float2 hb = __half22float2(hi);
-            const int64_t o = row * p.ldo + col;
-            if (c1ok) {
-                *reinterpret_cast<__half2*>(p.out_h + o) = hi;
-                if (p.out_l) *reinterpret_cast<__half2*>(p.out_l + o) = __floats2half2_rn(x0 - hb.x, x1 - hb.y);
-            } else if (c0ok) {
-                p.out_h[o] = __low2half(hi);
-                if (p.out_l) p.out_l[o] = __float2half_rn(x0 - hb.x);
+        } else {
+#pragma unroll 4
+            for (int rr = 0; rr < 32; rr += 2) {
+                const int64_t row = row0 + rr + half;
+                if (row >= M) continue;
+                float x0 = stg[(rr + half) * kStageLd + cp] + b0;
+                float x1 = stg[(rr + half) * kStageLd + cp + 1] + b1;
+                if (EPI == EPI_GELU_F16X) {
+                    x0 = gelu_fast(x0);
+                    x1 = gelu_fast(x1);
+                }
+                const __half2 hi = __floats2half2_rn(x0, x1);
+                const float2 hb = __half22float2(hi);
+                const int64_t o = row * p.ldo + col;
+                if (c1ok) {
+                    *reinterpret_cast<__half2*>(p.out_h + o) = hi;
+                    if (p.out_l) *reinterpret_cast<__half2*>(p.out_l + o) = __floats2half2_rn(x0 - hb.x, x1 - hb.y);
+                } else if (c0ok) {
+                    p.out_h[o] = __low2half(hi);
+                    if (p.out_l) p.out_l[o] = __float2half_rn(x0 - hb.x);
+                }
             }
         }
     } else {
@@ -146,35 +299,89 @@ __device__ __forceinline__ void epilogue_coalesced(const GemmEpiParams& p, int64
         const bool cok = col < N;
         const float b = (p.bias && cok) ? __ldg(p.bias + col) : 0.0f;
         float* out = p.out_f32 + row0 * p.ldo + col;
-        // all global loads of the chunk are issued before any use (32 in flight per lane)
-        float extra[32];
-        if (EPI == EPI_RESID || (EPI == EPI_GELU_PE && p.pe)) {
-            int pr = 0;
-            if (EPI == EPI_GELU_PE) pr = (int)(row0 % p.lw);  // window position of row0; advanced with wrap below
+        if (full) {
+            // all global loads of the chunk are issued before any use (32 in flight per lane)
+            if (EPI == EPI_RESID) {
+                float extra[32];  // all residual loads in flight before any use
 #pragma unroll
-            for (int rr = 0; rr < 32; ++rr) {
-                const bool ok = cok && row0 + rr < M;
-                if (EPI == EPI_RESID) {
-                    extra[rr] = ok ? out[rr * p.ldo] : 0.0f;
-                } else {
-                    extra[rr] = ok ? __ldg(p.pe + (int64_t)pr * p.ldo + col) : 0.0f;
-                    if (++pr == p.lw) pr = 0;
+                for (int rr = 0; rr < 32; ++rr) extra[rr] = out[rr * p.ldo];
+#pragma unroll
+                for (int rr = 0; rr < 32; ++rr) out[rr * p.ldo] = stg[rr * kStageLd + lane] + b + extra[rr];
+            } else {
+                int pr = (int)(row0 % p.lw);  // window position of row0 (PE table is L2-resident)
+#pragma unroll 8
+                for (int rr = 0; rr < 32; ++rr) {
+                    float x = stg[rr * kStageLd + lane] + b;
+                    if (EPI == EPI_GELU_PE) {
+                        x = gelu_fast(x);
+                        if (p.pe) x += __ldg(p.pe + (int64_t)pr * p.ldo + col);
+                        if (++pr == p.lw) pr = 0;
+                    }
+                    out[rr * p.ldo] = x;
                 }
             }
-        }
+        } else {
+            float extra[32];
+            if (EPI == EPI_RESID || (EPI == EPI_GELU_PE && p.pe)) {
+                int pr = 0;
+                if (EPI == EPI_GELU_PE) pr = (int)(row0 % p.lw);
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) {
-            if (!cok || row0 + rr >= M) continue;
-            float x = stg[rr * kStageLd + lane] + b;
-            if (EPI == EPI_GELU_PE) {
-                x = gelu_erf(x);
-                if (p.pe) x += extra[rr];
+                for (int rr = 0; rr < 32; ++rr) {
+                    const bool ok = cok && row0 + rr < M;
+                    if (EPI == EPI_RESID) {
+                        extra[rr] = ok ? out[rr * p.ldo] : 0.0f;
+                    } else {
+                        extra[rr] = ok ? __ldg(p.pe + (int64_t)pr * p.ldo + col) : 0.0f;
+                        if (++pr == p.lw) pr = 0;
+                    }
+                }
             }
-            if (EPI == EPI_RESID) x += extra[rr];
-            out[rr * p.ldo] = x;
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr) {
+                if (!cok || row0 + rr >= M) continue;
+                float x = stg[rr * kStageLd + lane] + b;
+                if (EPI == EPI_GELU_PE) {
+                    x = gelu_fast(x);
+                    if (p.pe) x += extra[rr];
+                }
+                if (EPI == EPI_RESID) x += extra[rr];
+                out[rr * p.ldo] = x;
+            }
         }
     }
     __syncwarp();
+}
+
+// Residual epilogue (resid += acc + bias) for a 32x32 chunk whose residual
+// values were prefetched by the caller (res[rr] = out[row0 + rr][col0 + lane]).
+__device__ __forceinline__ void epilogue_resid_pref(const GemmEpiParams& p, int64_t row0, int64_t col0, int64_t M,
+                                                    int64_t N, const uint32_t (&r)[32], const float (&res)[32],
+                                                    float* stg) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) stg[lane * kStageLd + j] = __uint_as_float(r[j]);
+    __syncwarp();
+    const int64_t col = col0 + lane;
+    const bool cok = col < N;
+    const float b = (p.bias && cok) ? __ldg(p.bias + col) : 0.0f;
+    float* out = p.out_f32 + row0 * p.ldo + col;
+    if (cok && row0 + 32 <= M) {
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) out[rr * p.ldo] = stg[rr * kStageLd + lane] + b + res[rr];
+    } else {
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr)
+            if (cok && row0 + rr < M) out[rr * p.ldo] = stg[rr * kStageLd + lane] + b + res[rr];
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void resid_prefetch(const GemmEpiParams& p, int64_t row0, int64_t col0, int64_t M,
+                                               int64_t N, float (&res)[32]) {
+    const int64_t col = col0 + (threadIdx.x & 31);
+    const float* src = p.out_f32 + row0 * p.ldo + col;
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) res[rr] = (col < N && row0 + rr < M) ? src[rr * p.ldo] : 0.0f;
 }
 
 template <int BN, int NA, int NB, int EPI>
@@ -500,13 +707,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int64_t t = cluster; t < tiles; t += nclusters) {
             const int64_t m0 = (t / tiles_n) * 256 + rank * 128;
             const int64_t n0 = (t % tiles_n) * BN;
-            mbar_wait(&tfull[acc], acc_phase);
-            tc_fence_after();
             const int64_t row = m0 + quad * 32 + lane;
             const uint32_t taddr = tmem_base + ((quad * 32) << 16) + acc * BN;
             // this warp's column group; the next chunk's TMEM load overlaps the
             // current chunk's epilogue math (double-buffered registers)
             const int cbeg = cg * (BN / kEpiGroups), cend = cbeg + BN / kEpiGroups;
+            if (EPI == EPI_RESID) {
+                // residual reads do not depend on the MMA: the first chunk's are
+                // issued before waiting for the accumulator, each next chunk's
+                // before the current chunk's stores
+                float res[32], nxt[32];
+                resid_prefetch(p, row - lane, n0 + cbeg, M, N, res);
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+#pragma unroll 1
+                for (int c0 = cbeg; c0 < cend; c0 += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(taddr + c0, r);
+                    if (c0 + 32 < cend) resid_prefetch(p, row - lane, n0 + c0 + 32, M, N, nxt);
+                    tmem_ld_wait();
+                    if (n0 + c0 < N) epilogue_resid_pref(p, row - lane, n0 + c0, M, N, r, res, stagebuf);
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) res[u] = nxt[u];
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+                continue;
+            }
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
             uint32_t r[2][32];
             tmem_ld32(taddr + cbeg, r[0]);
             tmem_ld_wait();

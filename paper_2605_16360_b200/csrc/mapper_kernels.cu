@@ -17,7 +17,6 @@
 namespace pkv {
 namespace {
 
-__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 
 __device__ __forceinline__ void store_split(__half* hi, __half* lo, int64_t i, float v) {
     const __half h = __float2half_rn(v);
@@ -94,7 +93,7 @@ __global__ void conv1_im2col_kernel(WinSrc src, const float* __restrict__ inv_me
                 acc = fmaf(wr[ci * 3 + 1], xr[1], acc);
                 acc = fmaf(wr[ci * 3 + 2], xr[2], acc);
             }
-            sz[tt * mid + c] = (t >= 0 && t < src.Lw) ? gelu_erf(acc) : 0.0f;
+            sz[tt * mid + c] = (t >= 0 && t < src.Lw) ? sm100::gelu_fast(acc) : 0.0f;
         }
     }
     __syncthreads();

@@ -5,8 +5,9 @@
 //   pass 1 (score_lse_kernel):  S = Q·Kᵀ (M = 128 queries, N = 256 keys) into
 //     double-buffered TMEM; 16 softmax warps (4 column segments x 4 TMEM lane
 //     quadrants) keep an online (max, Σexp2) per row segment in registers,
-//     merged through smem at the end; 1 in 4 exponentials is evaluated as a
-//     degree-4 polynomial on the FMA pipe to offload MUFU (FA4-style); writes
+//     merged through smem at the end; ~7 in 16 exponentials are evaluated as a
+//     degree-3 polynomial on the FMA pipe to offload MUFU (FA4-style), with
+//     the integer row max folded into the range reduction; writes
 //     lse[q] and the bf16 triple (hi, mid, lo) of λ_q = √d·lse_q.
 //   pass 2 (score_pool_kernel): S' = K·Qᵀ − λ (two M = 128 key blocks = 256
 //     keys per CTA, N = 128 queries per tile), the −λ_q column folded into the
@@ -32,9 +33,10 @@ constexpr float kLog2e = 1.4426950408889634f;
 template <int D>
 struct P1 {
     static constexpr int kBQ = 128, kBK = 256;
-    static constexpr int kSegs = 4;  // column segments of 64
+    static constexpr int kSegs = 4;  // column segments per tile (one warp per segment and TMEM lane quadrant)
+    static constexpr int kSegCols = kBK / kSegs;
     static constexpr int kSoftWarps = 4 * kSegs;
-    static constexpr int kThreads = 128 + 32 * kSoftWarps;
+    static constexpr int kThreads = 64 + 32 * kSoftWarps;  // warp 0 TMA, warp 1 TMEM+MMA
     static constexpr int kPanels = D / 64;
     static constexpr int kQBytes = kBQ * D * 2;
     static constexpr int kKBytes = kBK * D * 2;
@@ -80,6 +82,69 @@ __device__ __forceinline__ void write_lam(__nv_bfloat16* dst, float lam) {
 #pragma unroll
     for (int u = 3; u < 8; ++u) v[u] = __float2bfloat16_rn(0.0f);
     *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
+}
+
+// One 64-column chunk of a softmax row segment: online (max, Σexp2) update.
+// valid = number of leading columns that count (masked tail / causal diagonal).
+template <int kPolyPairs>
+__device__ __forceinline__ void lse_chunk(const uint32_t (&ra)[32], const uint32_t (&rb)[32], int valid, float c_log2,
+                                          float& m, float& lsum) {
+    float v[64];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+        v[u] = __uint_as_float(ra[u]);
+        v[32 + u] = __uint_as_float(rb[u]);
+    }
+    const bool masked = __any_sync(0xffffffffu, valid < 64);  // warp-uniform: tail / diagonal tiles
+    if (masked) {
+#pragma unroll
+        for (int u = 0; u < 64; ++u) v[u] = (u < valid) ? v[u] : -INFINITY;
+    }
+    // max as a tree (8 independent FMNMX3 chains) to keep the dependency short
+    float mt[8];
+#pragma unroll
+    for (int t8 = 0; t8 < 8; ++t8) mt[t8] = fmaxf(v[t8], v[t8 + 8]);
+#pragma unroll
+    for (int u = 16; u < 64; u += 16)
+#pragma unroll
+        for (int t8 = 0; t8 < 8; ++t8) mt[t8] = max3f(mt[t8], v[u + t8], v[u + t8 + 8]);
+    const float cm = max3f(max3f(mt[0], mt[1], mt[2]), max3f(mt[3], mt[4], mt[5]), fmaxf(mt[6], mt[7]));
+    // integer running max (log2 domain): lets the polynomial path fold the
+    // offset into its range reduction (ex2_poly2_fused)
+    const float mn = fmaxf(m, ceilf(cm * c_log2));
+    if (mn == -INFINITY) return;
+    // packed fp32x2: FFMA2 for the arguments, FADD2 for the sums; of the 32
+    // pairs, kPolyPairs go through the FMA-pipe polynomial, spread evenly
+    // (Bresenham), the rest through MUFU. Masked chunks take the MUFU path only.
+    const uint64_t cc = pack2(c_log2, c_log2), nm = pack2(-mn, -mn);
+    const uint64_t mp = pack2(12582912.0f - mn, 12582912.0f - mn);
+    uint64_t acc0 = pack2(0.0f, 0.0f), acc1 = acc0;
+    if (!masked) {
+#pragma unroll
+        for (int pr = 0; pr < 32; ++pr) {
+            const uint64_t s2 = pack2(v[2 * pr], v[2 * pr + 1]);
+            uint64_t e;
+            if (((pr + 1) * kPolyPairs) / 32 != (pr * kPolyPairs) / 32) {
+                e = ex2_poly2_fused(s2, cc, mp);
+            } else {
+                const float2 x = unpack2(ffma2(s2, cc, nm));
+                e = pack2(ex2(x.x), ex2(x.y));
+            }
+            if (pr & 1) acc1 = fadd2(acc1, e);
+            else acc0 = fadd2(acc0, e);
+        }
+    } else {
+#pragma unroll
+        for (int pr = 0; pr < 32; ++pr) {
+            const float2 x = unpack2(ffma2(pack2(v[2 * pr], v[2 * pr + 1]), cc, nm));
+            const uint64_t e = pack2(ex2(x.x), ex2(x.y));
+            if (pr & 1) acc1 = fadd2(acc1, e);
+            else acc0 = fadd2(acc0, e);
+        }
+    }
+    const float2 ssum = unpack2(fadd2(acc0, acc1));
+    lsum = lsum * ex2(m - mn) + (ssum.x + ssum.y);
+    m = mn;
 }
 
 // ---------------------------------------------------------------- pass 1 --
@@ -128,7 +193,7 @@ __global__ void __launch_bounds__(P1<D>::kThreads, 1)
         }
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -169,70 +234,45 @@ __global__ void __launch_bounds__(P1<D>::kThreads, 1)
             }
             __syncwarp();
         }
-    } else if (warp >= 4) {
+    } else {
         const uint32_t quad = warp & 3;
-        const int seg = (warp - 4) >> 2;  // 64-column segment of the 256-key tile
+        const int seg = (warp - 2) >> 2;  // column segment of the 256-key tile (quad = warp % 4)
         const int r = quad * 32 + lane;
         const int q = q0 + r;
         const int kmax = causal ? (q + off + 1 < Nk ? q + off + 1 : Nk) : Nk;  // keys [0, kmax) allowed
         float m = -INFINITY, lsum = 0.0f;  // m in the log2 (scaled) domain
+        constexpr int kChunks = C::kSegCols / 64;
         for (int j = 0; j < n_kv; ++j) {
             const int sb = j & 1;
             mbar_wait(&s_full[sb], (j >> 1) & 1);
             tc_fence_after();
-            const uint32_t base = tmem + ((quad * 32) << 16) + sb * C::kBK + seg * 64;
+            const uint32_t base = tmem + ((quad * 32) << 16) + sb * C::kBK + seg * C::kSegCols;
             uint32_t ra[32], rb[32];
             tmem_ld32(base, ra);
             tmem_ld32(base + 32, rb);
             tmem_ld_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s_empty[sb]);
-            const int valid = kmax - (j * C::kBK + seg * 64);  // columns [0, valid) of this segment count
-            float v[64];
 #pragma unroll
-            for (int u = 0; u < 32; ++u) {
-                v[u] = __uint_as_float(ra[u]);
-                v[32 + u] = __uint_as_float(rb[u]);
-            }
-            if (__any_sync(0xffffffffu, valid < 64)) {  // warp-uniform: only tail / diagonal tiles
+            for (int c = 0; c < kChunks; ++c) {
+                uint32_t na[32], nb[32];
+                if (c + 1 < kChunks) {  // prefetch the next 64 columns while this chunk computes
+                    tmem_ld32(base + 64 * (c + 1), na);
+                    tmem_ld32(base + 64 * (c + 1) + 32, nb);
+                } else {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&s_empty[sb]);
+                }
+                lse_chunk<kPolyPairs>(ra, rb, kmax - (j * C::kBK + seg * C::kSegCols + 64 * c), c_log2, m, lsum);
+                if (c + 1 < kChunks) {
+                    tmem_ld_wait();
 #pragma unroll
-                for (int u = 0; u < 64; ++u) v[u] = (u < valid) ? v[u] : -INFINITY;
-            }
-            // max as a tree (8 independent FMNMX3 chains) to keep the dependency short
-            float mt[8];
-#pragma unroll
-            for (int t8 = 0; t8 < 8; ++t8) mt[t8] = fmaxf(v[t8], v[t8 + 8]);
-#pragma unroll
-            for (int u = 16; u < 64; u += 16)
-#pragma unroll
-                for (int t8 = 0; t8 < 8; ++t8) mt[t8] = max3f(mt[t8], v[u + t8], v[u + t8 + 8]);
-            const float cm = max3f(max3f(mt[0], mt[1], mt[2]), max3f(mt[3], mt[4], mt[5]), fmaxf(mt[6], mt[7]));
-            const float mn = fmaxf(m, cm * c_log2);
-            if (mn == -INFINITY) continue;
-            // packed fp32x2: FFMA2 for the arguments, FADD2 for the sums; of every
-            // 8 pairs, kPolyPairs go through the FMA-pipe polynomial, the rest MUFU
-            const uint64_t cc = pack2(c_log2, c_log2), nm = pack2(-mn, -mn);
-            uint64_t acc0 = pack2(0.0f, 0.0f), acc1 = acc0;
-#pragma unroll
-            for (int u = 0; u < 64; u += 16) {
-#pragma unroll
-                for (int pr = 0; pr < 8; ++pr) {
-                    const uint64_t a = ffma2(pack2(v[u + 2 * pr], v[u + 2 * pr + 1]), cc, nm);
-                    uint64_t e;
-                    if ((pr * kPolyPairs) % 8 + kPolyPairs >= 8 || (kPolyPairs == 8)) {
-                        e = ex2_poly2_d3(a);
-                    } else {
-                        const float2 x = unpack2(a);
-                        e = pack2(ex2(x.x), ex2(x.y));
+                    for (int u = 0; u < 32; ++u) {
+                        asm volatile("" : "+r"(na[u]), "+r"(nb[u]));  // pin the reads after wait::ld
+                        ra[u] = na[u];
+                        rb[u] = nb[u];
                     }
-                    if (pr & 1) acc1 = fadd2(acc1, e);
-                    else acc0 = fadd2(acc0, e);
                 }
             }
-            const float2 ssum = unpack2(fadd2(acc0, acc1));
-            lsum = lsum * ex2(m - mn) + (ssum.x + ssum.y);
-            m = mn;
         }
         part[seg * C::kBQ + r] = make_float2(m, lsum);
         named_bar_sync(1, 32 * C::kSoftWarps);
@@ -254,7 +294,7 @@ __global__ void __launch_bounds__(P1<D>::kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 2) {
+    if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
@@ -471,12 +511,13 @@ template <int D>
 void run_lse(const ScoreShape& s, const void* q, const void* k, float* lse, __nv_bfloat16* lam, cudaStream_t st) {
     using C = P1<D>;
     static bool once = false;
-    static int poly = 3;
+    static int poly = 10;
+    using KernT = decltype(&score_lse_kernel<D, 12>);
+    static KernT table[5] = {score_lse_kernel<D, 6>, score_lse_kernel<D, 8>, score_lse_kernel<D, 10>,
+                             score_lse_kernel<D, 12>, score_lse_kernel<D, 14>};
     if (!once) {
-        set_smem(score_lse_kernel<D, 2>, C::kSmem);
-        set_smem(score_lse_kernel<D, 3>, C::kSmem);
-        set_smem(score_lse_kernel<D, 4>, C::kSmem);
-        if (const char* e = getenv("PKV_POLY_PAIRS")) poly = atoi(e);  // tuning knob: 2..4 of 8 pairs
+        for (KernT k : table) set_smem(k, C::kSmem);
+        if (const char* e = getenv("PKV_POLY_PAIRS")) poly = atoi(e);  // tuning knob: 6..14 of 32 pairs
         once = true;
     }
     const CUtensorMap tq = make_tmap_3d(q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, s.Nq, s.L * s.Hq, D * 2, D * 2 * s.Nq,
@@ -484,7 +525,8 @@ void run_lse(const ScoreShape& s, const void* q, const void* k, float* lse, __nv
     const CUtensorMap tk = make_tmap_3d(k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, s.Nk, s.L * s.Hkv, D * 2, D * 2 * s.Nk,
                                         64, C::kBK, 1, CU_TENSOR_MAP_SWIZZLE_128B);
     const dim3 grid((unsigned)((s.Nq + C::kBQ - 1) / C::kBQ), (unsigned)s.Hq, (unsigned)s.L);
-    auto kern = poly == 2 ? score_lse_kernel<D, 2> : (poly == 4 ? score_lse_kernel<D, 4> : score_lse_kernel<D, 3>);
+    const int pi = poly <= 6 ? 0 : poly <= 8 ? 1 : poly <= 10 ? 2 : poly <= 12 ? 3 : 4;
+    auto kern = table[pi];
     kern<<<grid, C::kThreads, C::kSmem, st>>>(tq, tk, (int)s.Hq, (int)s.Hkv, (int)s.Nq, (int)s.Nk, s.causal ? 1 : 0,
                                               kLog2e / sqrtf((float)D), lse, lam);
     check_launch("score_lse_kernel");

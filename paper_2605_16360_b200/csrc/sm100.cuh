@@ -102,8 +102,11 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
     return r;
 }
+// Relaxed: used to hand a TMEM accumulator back to the pair's MMA issuer after
+// tcgen05.wait::ld + tcgen05.fence::before_thread_sync; a .release arrive would
+// make every epilogue warp drain its global stores first (MEMBAR.ALL.GPU).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // 2-SM TMA: both CTAs of the pair load their half; the bytes complete on the
 // leader CTA's barrier (peer bit 24 of the shared::cluster address cleared).
@@ -174,6 +177,18 @@ __device__ __forceinline__ void mma_f16_ss(uint32_t tmem_d, uint64_t adesc, uint
         : "memory");
 }
 
+// D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16: A (M = 128 rows = TMEM lanes,
+// K packed two fp16 per 32-bit column) is read from tensor memory.
+__device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 // Arrive on an mbarrier once all previously issued tcgen05.mma of this thread
 // complete (implicitly fences before_thread_sync).
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -207,6 +222,16 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
         "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
         "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+
+// registers -> TMEM, 32x32b.x16 (16 columns).
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
         : "memory");
 }
 
@@ -279,6 +304,28 @@ __device__ __forceinline__ uint64_t ex2_poly2_d3(uint64_t x2) {
                  __int_as_float((__float_as_int(tf.y) << 23) + __float_as_int(pf.y)));
 }
 
+// 2^(c·s − m) for a pair, with an INTEGER row offset m folded into the range
+// reduction: mp = 1.5·2^23 − m (exact for |m| < 2^22). t = c·s + mp rounds to
+// 1.5·2^23 + j (j = rint(c·s − m)); mp − t is exact (Sterbenz), so f = c·s +
+// (mp − t) = (c·s − m) − j in one FFMA. 3 packed FP ops replace the scale
+// FFMA + 3-op magic-number reduction. j is clamped at −125 (2^f ≥ 0.7 keeps the exponent field ≥ 1; 2^f·2^−125 is
+// negligible); inputs must be finite. Degree-3 fit as ex2_poly2_d3.
+__device__ __forceinline__ uint64_t ex2_poly2_fused(uint64_t s2, uint64_t c2, uint64_t mp2) {
+    uint64_t t = ffma2(s2, c2, mp2);
+    float2 tf = unpack2(t);
+    tf.x = fmaxf(tf.x, 12582912.0f - 125.0f);
+    tf.y = fmaxf(tf.y, 12582912.0f - 125.0f);
+    t = pack2(tf.x, tf.y);
+    const uint64_t f = ffma2(s2, c2, fsub2(mp2, t));
+    uint64_t p = ffma2(pack2(0.05508868396282196f, 0.05508868396282196f), f,
+                       pack2(0.24260404706001282f, 0.24260404706001282f));
+    p = ffma2(p, f, pack2(0.6932762265205383f, 0.6932762265205383f));
+    p = ffma2(p, f, pack2(0.9999289512634277f, 0.9999289512634277f));
+    const float2 pf = unpack2(p);
+    return pack2(__int_as_float((__float_as_int(tf.x) << 23) + __float_as_int(pf.x)),
+                 __int_as_float((__float_as_int(tf.y) << 23) + __float_as_int(pf.y)));
+}
+
 // 2^x for x <= 0 on the FMA pipe (FA4-style MUFU offload): x = j + f with
 // j = rint(x), f ∈ [-0.5, 0.5]; 2^f by a degree-4 fit (max rel err 2.7e-6);
 // the exponent j is added as an integer.
@@ -303,6 +350,29 @@ __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Exact-erf GELU, 0.5·x·(1 + erf(x/√2)) (ops.cpp:225-234), branch-free:
+// erfc(z) = t·P5(t)·e^(−z²), t = 1/(1 + p·z) (Abramowitz–Stegun 7.1.26, |Δerf|
+// ≤ 1.5e-7); GELU = x − x·erfc/2 for x ≥ 0, x·erfc/2 otherwise. Max abs error
+// 5.3e-7 on [−8, 8] in fp32 (the fp32 erff form: 6.8e-7), 2 MUFU + ~14 FMA-pipe
+// ops instead of erff's two-range polynomial.
+__device__ __forceinline__ float gelu_fast(float x) {
+    const float z = fabsf(x) * 0.70710678118654752f;
+    const float t = rcp_approx(fmaf(0.3275911f, z, 1.0f));
+    float p = fmaf(1.061405429f, t, -1.453152027f);
+    p = fmaf(p, t, 1.421413741f);
+    p = fmaf(p, t, -0.284496736f);
+    p = fmaf(p, t, 0.254829592f);
+    const float e = ex2((z * -1.4426950408889634f) * z);
+    const float h = (0.5f * x) * ((p * t) * e);
+    return x >= 0.0f ? x - h : h;
 }
 
 // Three-input max (sm_100+).
