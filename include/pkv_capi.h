@@ -170,6 +170,48 @@ pkv_status pkv_pruner_run(pkv_pruner p, const void* q_dev, const void* kp_dev, c
 pkv_status pkv_pruner_run_host(pkv_pruner p, const void* q_host, const void* kp_host, const void* kt_host,
                                const void* vt_host, void* k_out_host, void* v_out_host, int32_t* idx_out_host,
                                void* stream);
+/* Dual-stream form (the proxy runs asynchronously to the target
+ * prefill): scoring + mapping (and, sharded by head, the score exchange) are
+ * enqueued on proxy_stream; select + compaction on target_stream, gated by an
+ * event recorded on proxy_stream. Arguments as pkv_pruner_run. */
+pkv_status pkv_pruner_run_dual(pkv_pruner p, const void* q_dev, const void* kp_dev, const void* kt_dev,
+                               const void* vt_dev, void* k_out_dev, void* v_out_dev, int32_t* idx_out_dev,
+                               float* scores_out_dev, void* proxy_stream, void* target_stream);
+
+/* ------------------------------------------------ multi-GPU -- */
+/* One context pruned by `world` ranks (one process per GPU). No reference
+ * code: the reference is single-threaded CPU; BASELINE.json configs[2,3].
+ *   PKV_SHARD_LAYER: rank owns a contiguous block of target layers (all KV
+ *     heads) and scores + maps the proxy layers they pair with (layer_pair is
+ *     monotone, mapper.cpp:44-49): no collective.
+ *   PKV_SHARD_HEAD: rank owns a contiguous group of target KV heads (all
+ *     layers); proxy layers are split across ranks and the mapped scores are
+ *     exchanged with one NCCL all-to-all (needs a pkv_comm).
+ * Per-slice results are bit-identical to the 1-GPU path. */
+#define PKV_SHARD_LAYER 0u
+#define PKV_SHARD_HEAD 1u
+#define PKV_COMM_ID_BYTES 128
+
+typedef struct pkv_comm_s* pkv_comm;
+
+/* The plan for (world, rank), host logic only: out8 = {t_lo, t_hi, h_lo,
+ * h_hi, p_lo, p_hi, a, b} (0-based, half-open): the rank selects and compacts
+ * target slices [t_lo, t_hi) x heads [h_lo, h_hi), scores and maps proxy
+ * layers [p_lo, p_hi), and produces mapped scores of target layers [a, b). */
+pkv_status pkv_shard_plan(const int64_t* geom5, int world, int rank, uint32_t mode, int64_t* out8);
+/* NCCL communicator (libnccl.so.2 is loaded at first use): rank 0 creates the
+ * id, the caller distributes it (e.g. over torch.distributed / MPI). */
+pkv_status pkv_comm_unique_id(uint8_t* id_out /* PKV_COMM_ID_BYTES */);
+pkv_status pkv_comm_create(pkv_ctx ctx, int world, int rank, const uint8_t* id, pkv_comm* out);
+void pkv_comm_destroy(pkv_comm c);
+/* A pruner for this rank's shard. comm may be NULL for PKV_SHARD_LAYER.
+ * Buffers passed to run / run_dual are then shard-local: q, kp the full proxy
+ * tensors (only layers [p_lo, p_hi) are read); kt, vt [t_hi-t_lo, h_hi-h_lo,
+ * N, dt]; k_out, v_out [.., .., K, dt]; idx_out [.., .., K]; scores_out
+ * [t_hi-t_lo, h_hi-h_lo, N]. */
+pkv_status pkv_pruner_create_sharded(pkv_ctx ctx, pkv_mapper m, int64_t Hq, int64_t dp, int64_t dt, int64_t N,
+                                     double rho, uint32_t score_flags, uint32_t shard_mode, int world, int rank,
+                                     pkv_comm comm, pkv_pruner* out);
 
 #ifdef __cplusplus
 }

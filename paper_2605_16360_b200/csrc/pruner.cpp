@@ -2,66 +2,136 @@
 // the caller's stream: score (proxy Q·Kᵀ, pooled) -> HybridAxialMapper
 // forward_full -> per-(layer, head) Top-K select (ascending indices) -> packed
 // KV gather. No host synchronisation inside pkv_pruner_run; the host-buffer
-// form adds the H2D / D2H copies and synchronises once at the end.
+// form adds the H2D / D2H copies and synchronises once at the end. A sharded
+// pruner (shard.cpp) runs the same steps on its part of one context.
 #include <cmath>
 #include <map>
+#include <memory>
 
 #include "mapper.h"
 #include "score.cuh"
+#include "shard.h"
 
 using namespace pkv;
 
 struct pkv_pruner_s {
     pkv_ctx ctx = nullptr;
     Mapper* mapper = nullptr;
-    ScoreShape score;
+    ScoreShape score;  // proxy layers [plan.p_lo, plan.p_hi) of the full proxy tensors
     bool reduce_max = true;
-    int64_t dt = 0, N = 0, K = 0, Ll = 0, Hl = 0;
-    std::vector<int64_t> unit_off;
-    std::vector<int> out_unit;
-    DevBuf lam, x, y, idx;
+    int64_t dt = 0, N = 0, K = 0, Ll = 0, Hl = 0, Hq = 0, dp = 0;
+    ShardPlan plan;  // world 1, layer mode = the whole context on one GPU
+    pkv_comm comm = nullptr;
+    std::vector<int64_t> unit_off;  // mapper units (unique proxy layers of target layers [a, b))
+    std::vector<int> out_unit;      // target layer a + i -> unit
+    DevBuf lam, x, y, y_local, idx;
     DevBuf host_in, host_out;  // device copies for the host-buffer form
+    cudaEvent_t ev = nullptr;
+    ~pkv_pruner_s() {
+        if (ev) cudaEventDestroy(ev);
+    }
+    int64_t slices() const { return (plan.t_hi - plan.t_lo) * (plan.h_hi - plan.h_lo); }
 };
+
+namespace {
+
+pkv_pruner make_pruner(pkv_ctx ctx, pkv_mapper m, int64_t Hq, int64_t dp, int64_t dt, int64_t N, double rho,
+                       uint32_t score_flags, uint32_t mode, int world, int rank, pkv_comm comm) {
+    require_ctx(ctx);
+    PKV_REQUIRE_VALUE(m != nullptr, "null pkv_mapper");
+    Mapper& mp = *m->m;
+    PKV_REQUIRE_VALUE(rho > 0.0 && rho <= 1.0, "retention ratio must be in (0, 1], got ", rho);
+    PKV_REQUIRE_VALUE(N > 0 && dt > 0, "context length and target head_dim must be positive");
+    ShardPlan plan = make_shard_plan(mp.geom, world, rank, mode);
+    PKV_REQUIRE_VALUE(mode != PKV_SHARD_HEAD || comm != nullptr, "head-group sharding needs a pkv_comm");
+    PKV_REQUIRE_VALUE(comm == nullptr || (comm->world == world && comm->rank == rank),
+                      "pkv_comm (world ", comm ? comm->world : 0, ", rank ", comm ? comm->rank : 0,
+                      ") does not match the shard (world ", world, ", rank ", rank, ")");
+    ScoreShape sc{plan.p_hi - plan.p_lo, Hq, mp.geom.proxy_heads, N, N, dp, (score_flags & PKV_SCORE_CAUSAL) != 0};
+    if (sc.L > 0) score_validate(sc);
+    auto p = std::make_unique<pkv_pruner_s>();
+    p->ctx = ctx;
+    p->mapper = &mp;
+    p->score = sc;
+    p->reduce_max = (score_flags & PKV_SCORE_REDUCE_SUM) == 0;
+    p->dt = dt;
+    p->N = N;
+    p->Hq = Hq;
+    p->dp = dp;
+    p->K = static_cast<int64_t>(std::ceil(rho * static_cast<double>(N)));  // pruning.cpp:17
+    p->Ll = mp.geom.target_layers;
+    p->Hl = mp.geom.target_heads;
+    p->plan = std::move(plan);
+    p->comm = comm;
+    std::map<int64_t, int> unit_of;
+    for (int64_t t = p->plan.a; t < p->plan.b; ++t) {
+        const int64_t ls = layer_pair(t + 1, mp.geom) - 1;
+        auto it = unit_of.find(ls);
+        if (it == unit_of.end()) {
+            it = unit_of.emplace(ls, static_cast<int>(p->unit_off.size())).first;
+            p->unit_off.push_back((ls - p->plan.p_lo) * mp.geom.proxy_heads * N);
+        }
+        p->out_unit.push_back(it->second);
+    }
+    return p.release();
+}
+
+// score -> map (-> exchange) on `ps`; select -> compact on `ts` (gated by an
+// event when the streams differ).
+void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, const void* vt, void* k_out,
+                void* v_out, int32_t* idx_out, float* scores_out, cudaStream_t ps, cudaStream_t ts) {
+    const ScoreShape& s = p->score;
+    const ShardPlan& pl = p->plan;
+    const int64_t slices = p->slices();
+    const int64_t n_map = pl.b - pl.a;
+    float* y_sel = scores_out ? scores_out : static_cast<float*>(p->y.get(static_cast<size_t>(slices * p->N) * 4));
+    float* y_map = pl.mode == PKV_SHARD_HEAD
+                       ? static_cast<float*>(p->y_local.get(static_cast<size_t>(std::max<int64_t>(n_map, 1) * p->Hl * p->N) * 4))
+                       : y_sel;
+    int32_t* idx = idx_out ? idx_out : static_cast<int32_t*>(p->idx.get(static_cast<size_t>(slices * p->K) * 4));
+    if (n_map > 0) {
+        // (1) proxy scoring of this rank's proxy layers: X [L, H_s, N]
+        const size_t q_off = static_cast<size_t>(pl.p_lo * p->Hq * p->N * p->dp) * 2;
+        const size_t k_off = static_cast<size_t>(pl.p_lo * s.Hkv * p->N * p->dp) * 2;
+        const auto* qp = static_cast<const uint8_t*>(q) + q_off;
+        const auto* kpp = static_cast<const uint8_t*>(kp) + k_off;
+        auto* lam = static_cast<__nv_bfloat16*>(p->lam.get(static_cast<size_t>(s.L * s.Hq * s.Nq) * 16));
+        auto* x = static_cast<float*>(p->x.get(static_cast<size_t>(s.L * s.Hkv * s.Nk) * 4));
+        launch_score_lse(s, qp, kpp, nullptr, lam, ps);
+        launch_score_pool(s, qp, kpp, lam, p->reduce_max, x, ps);
+        count_launch(p->ctx, 2);
+        // (2) mapper: Ŷ for target layers [a, b), all heads
+        p->mapper->run(x, p->unit_off, p->N, p->out_unit, y_map, ps);
+    }
+    // (2b) head-group sharding: every mapped row to the owner of its head
+    if (pl.mode == PKV_SHARD_HEAD) exchange_scores(p->comm, pl, p->Hl, p->N, y_map, y_sel, ps);
+    if (ts != ps) {
+        if (!p->ev) PKV_CUDA(cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming));
+        PKV_CUDA(cudaEventRecord(p->ev, ps));
+        PKV_CUDA(cudaStreamWaitEvent(ts, p->ev, 0));
+    }
+    if (slices == 0) return;
+    // (3) Top-K per (target layer, head): ascending retained indices
+    launch_topk_select(y_sel, slices, p->N, p->K, nullptr, idx, ts);
+    // (4) packed KV gather
+    launch_compact_kv(kt, vt, idx, slices, p->N, p->K, p->dt * 2, k_out, v_out, p->ctx->sm_count, ts);
+    count_launch(p->ctx, 2);
+}
+
+}  // namespace
 
 extern "C" {
 
 pkv_status pkv_pruner_create(pkv_ctx ctx, pkv_mapper m, int64_t Hq, int64_t dp, int64_t dt, int64_t N, double rho,
                              uint32_t score_flags, pkv_pruner* out) {
-    return guard([&] {
-        require_ctx(ctx);
-        PKV_REQUIRE_VALUE(m != nullptr, "null pkv_mapper");
-        Mapper& mp = *m->m;
-        PKV_REQUIRE_VALUE(rho > 0.0 && rho <= 1.0, "retention ratio must be in (0, 1], got ", rho);
-        PKV_REQUIRE_VALUE(N > 0 && dt > 0, "context length and target head_dim must be positive");
-        auto* p = new pkv_pruner_s();
-        p->ctx = ctx;
-        p->mapper = &mp;
-        p->score = ScoreShape{mp.geom.proxy_layers, Hq, mp.geom.proxy_heads, N, N, dp,
-                              (score_flags & PKV_SCORE_CAUSAL) != 0};
-        try {
-            score_validate(p->score);
-        } catch (...) {
-            delete p;
-            throw;
-        }
-        p->reduce_max = (score_flags & PKV_SCORE_REDUCE_SUM) == 0;
-        p->dt = dt;
-        p->N = N;
-        p->K = static_cast<int64_t>(std::ceil(rho * static_cast<double>(N)));  // pruning.cpp:17
-        p->Ll = mp.geom.target_layers;
-        p->Hl = mp.geom.target_heads;
-        std::map<int64_t, int> unit_of;
-        for (int64_t ll = 1; ll <= p->Ll; ++ll) {
-            const int64_t ls = layer_pair(ll, mp.geom);
-            auto it = unit_of.find(ls);
-            if (it == unit_of.end()) {
-                it = unit_of.emplace(ls, static_cast<int>(p->unit_off.size())).first;
-                p->unit_off.push_back((ls - 1) * mp.geom.proxy_heads * N);
-            }
-            p->out_unit.push_back(it->second);
-        }
-        *out = p;
-    });
+    return guard([&] { *out = make_pruner(ctx, m, Hq, dp, dt, N, rho, score_flags, PKV_SHARD_LAYER, 1, 0, nullptr); });
+}
+
+pkv_status pkv_pruner_create_sharded(pkv_ctx ctx, pkv_mapper m, int64_t Hq, int64_t dp, int64_t dt, int64_t N,
+                                     double rho, uint32_t score_flags, uint32_t shard_mode, int world, int rank,
+                                     pkv_comm comm, pkv_pruner* out) {
+    return guard(
+        [&] { *out = make_pruner(ctx, m, Hq, dp, dt, N, rho, score_flags, shard_mode, world, rank, comm); });
 }
 
 void pkv_pruner_destroy(pkv_pruner p) { delete p; }
@@ -73,23 +143,17 @@ pkv_status pkv_pruner_run(pkv_pruner p, const void* q, const void* kp, const voi
     return guard([&] {
         PKV_REQUIRE_VALUE(p != nullptr, "null pkv_pruner");
         auto st = static_cast<cudaStream_t>(stream);
-        const ScoreShape& s = p->score;
-        auto* lam = static_cast<__nv_bfloat16*>(p->lam.get(static_cast<size_t>(s.L * s.Hq * s.Nq) * 16));
-        auto* x = static_cast<float*>(p->x.get(static_cast<size_t>(s.L * s.Hkv * s.Nk) * 4));
-        float* y = scores_out ? scores_out
-                              : static_cast<float*>(p->y.get(static_cast<size_t>(p->Ll * p->Hl * p->N) * 4));
-        int32_t* idx = idx_out ? idx_out : static_cast<int32_t*>(p->idx.get(static_cast<size_t>(p->Ll * p->Hl * p->K) * 4));
-        // (1) proxy scoring: X [1, L_s, H_s, N]
-        launch_score_lse(s, q, kp, nullptr, lam, st);
-        launch_score_pool(s, q, kp, lam, p->reduce_max, x, st);
-        count_launch(p->ctx, 2);
-        // (2) mapper: Ŷ [1, L_l, H_l, N]
-        p->mapper->run(x, p->unit_off, p->N, p->out_unit, y, st);
-        // (3) Top-K per (target layer, head): ascending retained indices
-        launch_topk_select(y, p->Ll * p->Hl, p->N, p->K, nullptr, idx, st);
-        // (4) packed KV gather
-        launch_compact_kv(kt, vt, idx, p->Ll * p->Hl, p->N, p->K, p->dt * 2, k_out, v_out, p->ctx->sm_count, st);
-        count_launch(p->ctx, 2);
+        run_pruner(p, q, kp, kt, vt, k_out, v_out, idx_out, scores_out, st, st);
+    });
+}
+
+pkv_status pkv_pruner_run_dual(pkv_pruner p, const void* q, const void* kp, const void* kt, const void* vt,
+                               void* k_out, void* v_out, int32_t* idx_out, float* scores_out, void* proxy_stream,
+                               void* target_stream) {
+    return guard([&] {
+        PKV_REQUIRE_VALUE(p != nullptr, "null pkv_pruner");
+        run_pruner(p, q, kp, kt, vt, k_out, v_out, idx_out, scores_out, static_cast<cudaStream_t>(proxy_stream),
+                   static_cast<cudaStream_t>(target_stream));
     });
 }
 
@@ -98,12 +162,12 @@ pkv_status pkv_pruner_run_host(pkv_pruner p, const void* q_h, const void* kp_h, 
     return guard([&] {
         PKV_REQUIRE_VALUE(p != nullptr, "null pkv_pruner");
         auto st = static_cast<cudaStream_t>(stream);
-        const ScoreShape& s = p->score;
-        const size_t qb = static_cast<size_t>(s.L * s.Hq * s.Nq * s.d) * 2;
-        const size_t kpb = static_cast<size_t>(s.L * s.Hkv * s.Nk * s.d) * 2;
-        const size_t kvb = static_cast<size_t>(p->Ll * p->Hl * p->N * p->dt) * 2;
-        const size_t ob = static_cast<size_t>(p->Ll * p->Hl * p->K * p->dt) * 2;
-        const size_t ib = static_cast<size_t>(p->Ll * p->Hl * p->K) * 4;
+        const int64_t Ls = p->mapper->geom.proxy_layers, Hs = p->mapper->geom.proxy_heads;
+        const size_t qb = static_cast<size_t>(Ls * p->Hq * p->N * p->dp) * 2;
+        const size_t kpb = static_cast<size_t>(Ls * Hs * p->N * p->dp) * 2;
+        const size_t kvb = static_cast<size_t>(p->slices() * p->N * p->dt) * 2;
+        const size_t ob = static_cast<size_t>(p->slices() * p->K * p->dt) * 2;
+        const size_t ib = static_cast<size_t>(p->slices() * p->K) * 4;
         auto* in = static_cast<uint8_t*>(p->host_in.get(qb + kpb + 2 * kvb));
         auto* outb = static_cast<uint8_t*>(p->host_out.get(2 * ob + ib));
         PKV_CUDA(cudaMemcpyAsync(in, q_h, qb, cudaMemcpyHostToDevice, st));

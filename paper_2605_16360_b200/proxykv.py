@@ -24,7 +24,8 @@ __all__ = [
     "retention_count", "topk_select", "topk_mask", "apply_mask", "compact_kv", "score", "score_lse",
     "layer_pair", "window_offsets", "mapper_init_params", "ShapeError", "PkvValueError", "ConfigError",
     "CudaError", "NoDeviceError", "PkvError", "SCORE_REDUCE_MAX", "SCORE_REDUCE_SUM", "SCORE_CAUSAL",
-    "MAPPER_FP16", "MAPPER_FP16X2", "MAPPER_FP16X3",
+    "MAPPER_FP16", "MAPPER_FP16X2", "MAPPER_FP16X3", "SHARD_LAYER", "SHARD_HEAD", "ShardPlan", "shard_plan",
+    "Comm",
 ]
 
 SCORE_REDUCE_MAX = 0
@@ -33,6 +34,9 @@ SCORE_CAUSAL = 2
 MAPPER_FP16 = 1
 MAPPER_FP16X2 = 2
 MAPPER_FP16X3 = 3
+SHARD_LAYER = 0
+SHARD_HEAD = 1
+COMM_ID_BYTES = 128
 
 
 def _torch():
@@ -306,15 +310,77 @@ class Mapper:
     forward_pair = sliding_forward
 
 
+@dataclass(frozen=True)
+class ShardPlan:
+    """What one rank owns of one context (pkv_shard_plan; 0-based, half-open):
+    it selects and compacts target slices [t_lo, t_hi) x heads [h_lo, h_hi),
+    scores and maps proxy layers [p_lo, p_hi) and produces the mapped scores of
+    target layers [a, b) (all heads)."""
+    t_lo: int
+    t_hi: int
+    h_lo: int
+    h_hi: int
+    p_lo: int
+    p_hi: int
+    a: int
+    b: int
+
+
+def shard_plan(geom: ModelGeometry, world: int, rank: int, mode: int = SHARD_LAYER) -> ShardPlan:
+    """Host logic only (no device): the multi-GPU partition of SURVEY §8e."""
+    out = (ctypes.c_int64 * 8)()
+    check(lib().pkv_shard_plan(geom.as5(), world, rank, mode, out))
+    return ShardPlan(*[int(v) for v in out])
+
+
+class Comm:
+    """pkv_comm: NCCL communicator for head-group sharding. `uid` is the
+    PKV_COMM_ID_BYTES id from Comm.unique_id() on rank 0, distributed by the
+    caller (e.g. torch.distributed.broadcast_object_list)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(COMM_ID_BYTES)
+        check(lib().pkv_comm_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, ctx: Context, world: int, rank: int, uid: bytes):
+        h = ctypes.c_void_p()
+        check(lib().pkv_comm_create(ctx.h, world, rank, ctypes.create_string_buffer(uid, COMM_ID_BYTES),
+                                    ctypes.byref(h)))
+        self.h = h
+        self.world = world
+        self.rank = rank
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h and _lib._lib is not None:
+            _lib._lib.pkv_comm_destroy(h)
+            self.h = None
+
+
 class Pruner:
-    """pkv_pruner: score -> map -> select -> compact for one context shape."""
+    """pkv_pruner: score -> map -> select -> compact for one context shape.
+    With `shard=(mode, world, rank)` (and `comm` for SHARD_HEAD) the pruner
+    handles this rank's part of the context; buffers are then shard-local
+    (see pkv_pruner_create_sharded and `self.plan`)."""
 
     def __init__(self, mapper: Mapper, Hq: int, dp: int, dt: int, N: int, rho: float, *, reduce: str = "max",
-                 causal: bool = False):
+                 causal: bool = False, shard: Optional[Tuple[int, int, int]] = None, comm: Optional[Comm] = None):
         self.mapper = mapper
         flags = (SCORE_REDUCE_SUM if reduce == "sum" else SCORE_REDUCE_MAX) | (SCORE_CAUSAL if causal else 0)
         h = ctypes.c_void_p()
-        check(lib().pkv_pruner_create(mapper.ctx.h, mapper.h, Hq, dp, dt, N, float(rho), flags, ctypes.byref(h)))
+        if shard is None:
+            check(lib().pkv_pruner_create(mapper.ctx.h, mapper.h, Hq, dp, dt, N, float(rho), flags, ctypes.byref(h)))
+            self.plan = ShardPlan(0, mapper.geom.target_layers, 0, mapper.geom.target_heads, 0,
+                                  mapper.geom.proxy_layers, 0, mapper.geom.target_layers)
+        else:
+            mode, world, rank = shard
+            check(lib().pkv_pruner_create_sharded(mapper.ctx.h, mapper.h, Hq, dp, dt, N, float(rho), flags, mode,
+                                                  world, rank, comm.h if comm is not None else None,
+                                                  ctypes.byref(h)))
+            self.plan = shard_plan(mapper.geom, world, rank, mode)
+        self.comm = comm
         self.h = h
         self.k = int(lib().pkv_pruner_k(h))
         self.N = N
@@ -328,6 +394,12 @@ class Pruner:
     def run(self, q, kp, kt, vt, k_out, v_out, idx_out=None, scores_out=None, stream=None):
         check(lib().pkv_pruner_run(self.h, _ptr(q), _ptr(kp), _ptr(kt), _ptr(vt), _ptr(k_out), _ptr(v_out),
                                    _ptr(idx_out), _ptr(scores_out), _stream(stream)))
+
+    def run_dual(self, q, kp, kt, vt, k_out, v_out, idx_out=None, scores_out=None, *, proxy_stream, target_stream):
+        """Scoring + mapping on proxy_stream, select + compaction on target_stream."""
+        check(lib().pkv_pruner_run_dual(self.h, _ptr(q), _ptr(kp), _ptr(kt), _ptr(vt), _ptr(k_out), _ptr(v_out),
+                                        _ptr(idx_out), _ptr(scores_out), _stream(proxy_stream),
+                                        _stream(target_stream)))
 
     def run_host(self, q, kp, kt, vt, k_out, v_out, idx_out=None, stream=None):
         """Host (ideally pinned) torch tensors in and out; copies happen inside the call."""
