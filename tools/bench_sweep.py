@@ -1,0 +1,64 @@
+"""BASELINE.json configs[4]: KV-budget sweep (rho 10-50% x ctx 8k-128k) on
+Llama-3.1-8B target shapes (32 layers x 8 KV heads, head_dim 128, bf16): the
+select + compaction regime, HBM-bound. Per point: select (radix Top-K ->
+ascending indices) and compaction (packed K/V gather) timed with CUDA events
+on the launching stream (5 iterations after 3 warm-ups; inputs > L2 except
+the scores at 8k-16k, which the select reads once), algorithmic bytes per
+SURVEY.md §8(d), fraction of MEASURED_PEAKS.json HBM bandwidth.
+
+    python tools/bench_sweep.py [--out profiles/r01_sweep.json]
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2605_16360_b200 as P  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--out", default=None)
+a = ap.parse_args()
+Ll, Hl, dt = 32, 8, 128
+S = Ll * Hl
+hbm = bench.peaks()[0]
+ctx = P.Context(0)
+st = torch.cuda.current_stream()
+rows = []
+for N in (8192, 16384, 32768, 65536, 131072):
+    g = torch.Generator(device="cuda").manual_seed(N)
+    scores = torch.rand(S, N, device="cuda", generator=g)
+    kt = torch.randint(-30000, 30000, (S, N, dt), device="cuda", dtype=torch.int16, generator=g).view(torch.bfloat16)
+    vt = torch.randint(-30000, 30000, (S, N, dt), device="cuda", dtype=torch.int16, generator=g).view(torch.bfloat16)
+    for rho in (0.1, 0.2, 0.3, 0.4, 0.5):
+        K = P.retention_count(rho, N)
+        ko = torch.empty(S, K, dt, dtype=torch.bfloat16, device="cuda")
+        vo = torch.empty_like(ko)
+        sel = lambda: P.topk_select(scores, K, want_mask=False, ctx=ctx, stream=st)
+        _, idx = sel()
+        cmp = lambda: P.compact_kv(kt, vt, idx, ctx=ctx, stream=st, out=(ko, vo))
+        for _ in range(3):
+            sel()
+            cmp()
+        t_sel = bench.time_loop(sel, 5, st)
+        t_cmp = bench.time_loop(cmp, 5, st)
+        c = dict(Ll=Ll, Hl=Hl, N=N, rho=rho, dt=dt)
+        b_sel, b_cmp = bench.bytes_select(c), bench.bytes_compact(c)
+        r = dict(N=N, rho=rho, K=K, select_ms=t_sel, compact_ms=t_cmp,
+                 select_gbs=b_sel / t_sel / 1e6, compact_gbs=b_cmp / t_cmp / 1e6,
+                 combined_frac_hbm=(b_sel + b_cmp) / (t_sel + t_cmp) / 1e6 / hbm)
+        rows.append(r)
+        print(f"N={N:6d} rho={rho:.1f} K={K:6d}  select {t_sel:7.3f} ms {r['select_gbs']:7.0f} GB/s  "
+              f"compact {t_cmp:7.3f} ms {r['compact_gbs']:7.0f} GB/s  select+compact {100 * r['combined_frac_hbm']:.1f}% "
+              f"of {hbm:.0f} GB/s", flush=True)
+        del ko, vo, idx
+    del scores, kt, vt
+    torch.cuda.empty_cache()
+if a.out:
+    json.dump({"hbm_peak_gbs": hbm, "target": "Llama-3.1-8B (32L, 8KV, d128) bf16", "points": rows},
+              open(a.out, "w"), indent=1)
