@@ -8,7 +8,7 @@
 // (pruning.cpp:24-31), with -0.0 == +0.0 as in the reference's `!=`.
 //
 // One CTA (1024 threads) per slice; HBM-bound: the slice is read once from
-// HBM, the 3 later digit passes and the output pass hit L2 (slices of
+// HBM, the 2 later digit passes and the output pass hit L2 (slices of
 // 128-680 KB, whole score tensor 16-76 MB << 126 MB L2).
 #include "internal.h"
 
@@ -52,71 +52,83 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* warp_s
     return base + x - v;
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 1)
     topk_select_kernel(const float* __restrict__ scores, int64_t n, int64_t k, uint8_t* __restrict__ mask,
                        int32_t* __restrict__ idx) {
-    __shared__ uint32_t hist[256];
+    __shared__ uint32_t hist[4096 + kWarps];  // + one discard bin per warp
     __shared__ uint32_t warp_sums[kWarps];
     __shared__ uint32_t s_digit, s_above;
 
     const int64_t slice = blockIdx.x;
+    const uint32_t trash = 4096u + (threadIdx.x >> 5);
     const float* __restrict__ v = scores + slice * n;
     const bool vec4 = (n & 3) == 0;
     const int tid = threadIdx.x;
 
-    // ---- radix select of the k-th largest key, 4 digit passes of 8 bits
+    // ---- radix select of the k-th largest key: digits of 12, 12 and 8 bits.
+    // Wide first digits spread score rows that share a few exponent values
+    // over many bins (same-bin shared atomics serialise).
     uint32_t prefix = 0, pmask = 0, kr = (uint32_t)k;
-    for (int pass = 0; pass < 4; ++pass) {
-        const int shift = 24 - 8 * pass;
-        if (tid < 256) hist[tid] = 0;
+#pragma unroll 1
+    for (int pass = 0; pass < 3; ++pass) {
+        const int bits = pass < 2 ? 12 : 8;
+        const int shift = pass == 0 ? 20 : (pass == 1 ? 8 : 0);
+        const uint32_t nb = 1u << bits, dmask = nb - 1;
+        for (uint32_t j = tid; j < nb; j += kThreads) hist[j] = 0;
         __syncthreads();
+        auto add = [&](uint32_t key) {  // branch-free: non-candidates into the warp's discard bin
+            atomicAdd(&hist[(key & pmask) == prefix ? (key >> shift) & dmask : trash], 1u);
+        };
         if (vec4) {
             const float4* v4 = reinterpret_cast<const float4*>(v);
-            for (int64_t i = tid; i < (n >> 2); i += kThreads) {
-                const float4 f = v4[i];
-                const uint32_t k0 = order_key(f.x), k1 = order_key(f.y), k2 = order_key(f.z), k3 = order_key(f.w);
-                if ((k0 & pmask) == prefix) atomicAdd(&hist[(k0 >> shift) & 255u], 1u);
-                if ((k1 & pmask) == prefix) atomicAdd(&hist[(k1 >> shift) & 255u], 1u);
-                if ((k2 & pmask) == prefix) atomicAdd(&hist[(k2 >> shift) & 255u], 1u);
-                if ((k3 & pmask) == prefix) atomicAdd(&hist[(k3 >> shift) & 255u], 1u);
+            const int64_t n4 = n >> 2;
+            for (int64_t i0 = tid; i0 < n4; i0 += 2 * kThreads) {
+                float4 f[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+                    f[u] = (i0 + u * kThreads < n4) ? v4[i0 + u * kThreads] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    if (i0 + u * kThreads >= n4) break;
+                    add(order_key(f[u].x));
+                    add(order_key(f[u].y));
+                    add(order_key(f[u].z));
+                    add(order_key(f[u].w));
+                }
             }
         } else {
-            for (int64_t i = tid; i < n; i += kThreads) {
-                const uint32_t key = order_key(v[i]);
-                if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
-            }
+            for (int64_t i = tid; i < n; i += kThreads) add(order_key(v[i]));
         }
         __syncthreads();
-        if (tid < 32) {
-            // lane l owns bins 255-8l .. 248-8l (descending digit order)
-            uint32_t c[8], s = 0;
+        // thread t owns bins_per_thread consecutive bins in descending digit order
+        const uint32_t bpt = nb / kThreads;  // 4 (12-bit digits) or 0 (8-bit)
+        uint32_t c[4] = {0, 0, 0, 0}, sum = 0;
+        if (bpt) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                c[j] = hist[255 - (tid * 8 + j)];
-                s += c[j];
+            for (int j = 0; j < 4; ++j) {
+                c[j] = hist[nb - 1 - (tid * 4 + j)];
+                sum += c[j];
             }
-            uint32_t incl = s;
+        } else if ((uint32_t)tid < nb) {
+            c[0] = hist[nb - 1 - tid];
+            sum = c[0];
+        }
+        uint32_t total;
+        const uint32_t excl = block_excl_scan(sum, warp_sums, total);
+        if (excl < kr && kr <= excl + sum) {
+            uint32_t acc = excl;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (tid >= o) incl += y;
-            }
-            const uint32_t excl = incl - s;
-            if (excl < kr && kr <= incl) {
-                uint32_t acc = excl;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    if (acc < kr && kr <= acc + c[j]) {
-                        s_digit = 255u - (uint32_t)(tid * 8 + j);
-                        s_above = acc;
-                    }
-                    acc += c[j];
+            for (int j = 0; j < 4; ++j) {
+                if (acc < kr && kr <= acc + c[j]) {
+                    s_digit = nb - 1 - (uint32_t)(bpt ? tid * 4 + j : tid);
+                    s_above = acc;
                 }
+                acc += c[j];
             }
         }
         __syncthreads();
         prefix |= s_digit << shift;
-        pmask |= 0xFFu << shift;
+        pmask |= dmask << shift;
         kr -= s_above;
         __syncthreads();
     }
@@ -188,12 +200,162 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
 }
 
+// Rows of n <= kThreads * kItems * kCacheTiles (32768) elements: the row's
+// order keys are read once into registers (thread t holds the same
+// consecutive-8 groups the output pass uses) and the three digit passes and
+// the output pass run on them — one global read per element instead of four,
+// and no key recomputation (the uncached kernel is ALU-bound on it).
+constexpr int kCacheTiles = 4;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    topk_select_cached_kernel(const float* __restrict__ scores, int64_t n, int64_t k, uint8_t* __restrict__ mask,
+                              int32_t* __restrict__ idx) {
+    __shared__ uint32_t hist[4096 + kWarps];  // + one discard bin per warp
+    __shared__ uint32_t warp_sums[kWarps];
+    __shared__ uint32_t s_digit, s_above;
+    const int tid = threadIdx.x;
+    const int64_t slice = blockIdx.x;
+    const int nn = (int)n;
+    const uint32_t trash = 4096u + (uint32_t)(tid >> 5);
+    const float* __restrict__ v = scores + slice * n;
+    const int ntiles = (nn + kThreads * kItems - 1) / (kThreads * kItems);
+    uint32_t key[kCacheTiles][kItems];
+#pragma unroll
+    for (int t = 0; t < kCacheTiles; ++t) {
+        const int i0 = t * kThreads * kItems + tid * kItems;
+        if ((nn & 3) == 0 && i0 + kItems <= nn) {
+            const float4 a = __ldcs(reinterpret_cast<const float4*>(v + i0));
+            const float4 b = __ldcs(reinterpret_cast<const float4*>(v + i0 + 4));
+            key[t][0] = order_key(a.x);
+            key[t][1] = order_key(a.y);
+            key[t][2] = order_key(a.z);
+            key[t][3] = order_key(a.w);
+            key[t][4] = order_key(b.x);
+            key[t][5] = order_key(b.y);
+            key[t][6] = order_key(b.z);
+            key[t][7] = order_key(b.w);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kItems; ++j) key[t][j] = (i0 + j < nn) ? order_key(v[i0 + j]) : 0u;
+        }
+    }
+    // per tile: number of this thread's items that exist
+    auto nvalid = [&](int t) {
+        const int i0 = t * kThreads * kItems + tid * kItems;
+        const int r = nn - i0;
+        return r <= 0 ? 0 : (r >= kItems ? kItems : r);
+    };
+    uint32_t prefix = 0, pmask = 0, kr = (uint32_t)k;
+#pragma unroll 1
+    for (int pass = 0; pass < 3; ++pass) {
+        const int bits = pass < 2 ? 12 : 8;
+        const int shift = pass == 0 ? 20 : (pass == 1 ? 8 : 0);
+        const uint32_t nb = 1u << bits, dmask = nb - 1;
+        for (uint32_t j = tid; j < nb; j += kThreads) hist[j] = 0;
+        __syncthreads();
+        // branch-free: non-candidates count into this warp's discard bin
+        // (ATOMS.POPC.INC merges a warp's same-address increments)
+#pragma unroll
+        for (int t = 0; t < kCacheTiles; ++t) {
+            if (t >= ntiles) break;
+            const int nv = nvalid(t);
+#pragma unroll
+            for (int j = 0; j < kItems; ++j) {
+                const bool ok = j < nv && (key[t][j] & pmask) == prefix;
+                atomicAdd(&hist[ok ? (key[t][j] >> shift) & dmask : trash], 1u);
+            }
+        }
+        __syncthreads();
+        const uint32_t bpt = nb / kThreads;
+        uint32_t c[4] = {0, 0, 0, 0}, sum = 0;
+        if (bpt) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                c[j] = hist[nb - 1 - (tid * 4 + j)];
+                sum += c[j];
+            }
+        } else if ((uint32_t)tid < nb) {
+            c[0] = hist[nb - 1 - tid];
+            sum = c[0];
+        }
+        uint32_t total;
+        const uint32_t excl = block_excl_scan(sum, warp_sums, total);
+        if (excl < kr && kr <= excl + sum) {
+            uint32_t acc = excl;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (acc < kr && kr <= acc + c[j]) {
+                    s_digit = nb - 1 - (uint32_t)(bpt ? tid * 4 + j : tid);
+                    s_above = acc;
+                }
+                acc += c[j];
+            }
+        }
+        __syncthreads();
+        prefix |= s_digit << shift;
+        pmask |= dmask << shift;
+        kr -= s_above;
+        __syncthreads();
+    }
+    const uint32_t kth = prefix, ties_taken = kr;
+    uint32_t sel_base = 0, tie_base = 0;
+    uint8_t* __restrict__ mrow = mask ? mask + slice * n : nullptr;
+    int32_t* __restrict__ irow = idx ? idx + slice * k : nullptr;
+#pragma unroll
+    for (int t = 0; t < kCacheTiles; ++t) {
+        if (t >= ntiles) break;
+        const int i0 = t * kThreads * kItems + tid * kItems;
+        const int nv = nvalid(t);
+        uint32_t gt = 0, eq = 0;
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) {
+            const uint32_t in = (uint32_t)(j < nv);
+            gt |= (in & (uint32_t)(key[t][j] > kth)) << j;
+            eq |= (in & (uint32_t)(key[t][j] == kth)) << j;
+        }
+        // one scan of (#greater, #equal) packed in 16-bit halves (< 8192 each);
+        // ties go to the lowest indices: this thread takes the first
+        // min(ties left - equal keys before it, #equal) of its own
+        uint32_t tot;
+        const uint32_t excl = block_excl_scan((uint32_t)__popc(gt) | ((uint32_t)__popc(eq) << 16), warp_sums, tot);
+        const uint32_t gt_excl = excl & 0xFFFFu, eq_excl = excl >> 16;
+        const uint32_t ties_left = ties_taken - min(ties_taken, tie_base);
+        const uint32_t tb = min(ties_left, eq_excl);                       // ties taken before this thread
+        const uint32_t mine = min(ties_left - tb, (uint32_t)__popc(eq));   // ties this thread takes
+        uint32_t sel = gt, e = eq;
+        for (uint32_t m = 0; m < mine; ++m) {  // lowest `mine` equal keys
+            sel |= e & (0u - e);
+            e &= e - 1;
+        }
+        if (irow) {
+            uint32_t pos = sel_base + gt_excl + tb, b = sel;
+            while (b) {
+                const int jj = __ffs(b) - 1;
+                irow[pos++] = i0 + jj;
+                b &= b - 1;
+            }
+        }
+        if (mrow) {
+#pragma unroll
+            for (int jj = 0; jj < kItems; ++jj)
+                if (jj < nv) mrow[i0 + jj] = (uint8_t)((sel >> jj) & 1u);
+        }
+        const uint32_t tot_gt = tot & 0xFFFFu, tot_eq = tot >> 16;
+        sel_base += tot_gt + min(ties_left, tot_eq);
+        tie_base += tot_eq;
+    }
+}
+
 }  // namespace
 
 void launch_topk_select(const float* scores, int64_t slices, int64_t n, int64_t k, uint8_t* mask, int32_t* idx,
                         cudaStream_t st) {
     if (slices == 0) return;
-    topk_select_kernel<<<(unsigned)slices, kThreads, 0, st>>>(scores, n, k, mask, idx);
+    if (n <= (int64_t)kThreads * kItems * kCacheTiles) {
+        topk_select_cached_kernel<<<(unsigned)slices, kThreads, 0, st>>>(scores, n, k, mask, idx);
+    } else {
+        topk_select_kernel<<<(unsigned)slices, kThreads, 0, st>>>(scores, n, k, mask, idx);
+    }
     check_launch("topk_select_kernel");
 }
 
