@@ -166,7 +166,11 @@ pkv_status pkv_pruner_run(pkv_pruner p, const void* q_dev, const void* kp_dev, c
                           const void* vt_dev, void* k_out_dev, void* v_out_dev, int32_t* idx_out_dev,
                           float* scores_out_dev, void* stream);
 /* Same with host buffers: H2D of the inputs and D2H of the outputs are part
- * of the call (the reference-facing end-to-end form). */
+ * of the call (the reference-facing end-to-end form). The copies run on the
+ * pruner's own stream, overlapped with compute: the proxy Q/K in four
+ * layer chunks (each chunk's scoring starts when it lands), then the target
+ * KV (consumed only by select + compaction, after the mapper). Pinned host
+ * memory makes the copies asynchronous. */
 pkv_status pkv_pruner_run_host(pkv_pruner p, const void* q_host, const void* kp_host, const void* kt_host,
                                const void* vt_host, void* k_out_host, void* v_out_host, int32_t* idx_out_host,
                                void* stream);

@@ -262,9 +262,10 @@ __device__ __forceinline__ void epilogue_coalesced(const GemmEpiParams& p, int64
             for (int rr = 0; rr < 32; rr += 2) {
                 float x0 = stg[(rr + half) * kStageLd + cp] + b0;
                 float x1 = stg[(rr + half) * kStageLd + cp + 1] + b1;
-                if (EPI == EPI_GELU_F16X) {
-                    x0 = gelu_fast(x0);
-                    x1 = gelu_fast(x1);
+                if (EPI == EPI_GELU_F16X) {  // packed FFMA2/FMUL2 form of gelu_fast
+                    const float2 g = gelu_fast2(x0, x1);
+                    x0 = g.x;
+                    x1 = g.y;
                 }
                 const __half2 hi = __floats2half2_rn(x0, x1);
                 const float2 hb = __half22float2(hi);

@@ -4,6 +4,7 @@
 // KV gather. No host synchronisation inside pkv_pruner_run; the host-buffer
 // form adds the H2D / D2H copies and synchronises once at the end. A sharded
 // pruner (shard.cpp) runs the same steps on its part of one context.
+#include <algorithm>
 #include <cmath>
 #include <map>
 #include <memory>
@@ -27,13 +28,29 @@ struct pkv_pruner_s {
     DevBuf lam, x, y, y_local, idx;
     DevBuf host_in, host_out;  // device copies for the host-buffer form
     cudaEvent_t ev = nullptr;
+    // host-buffer form: copy stream + events (proxy layer chunks, target KV)
+    cudaStream_t copy_st = nullptr;
+    static constexpr int kChunks = 4;
+    cudaEvent_t ev_in[kChunks + 2] = {};
     ~pkv_pruner_s() {
         if (ev) cudaEventDestroy(ev);
+        for (cudaEvent_t e : ev_in)
+            if (e) cudaEventDestroy(e);
+        if (copy_st) cudaStreamDestroy(copy_st);
     }
     int64_t slices() const { return (plan.t_hi - plan.t_lo) * (plan.h_hi - plan.h_lo); }
 };
 
 namespace {
+
+// Inputs arriving from the host (pkv_pruner_run_host): scoring of proxy-layer
+// chunk c waits for ev_chunk[c]; select + compaction wait for ev_kv.
+struct HostArrival {
+    int chunks = 0;
+    int64_t chunk_layers = 0;
+    const cudaEvent_t* ev_chunk = nullptr;
+    cudaEvent_t ev_kv = nullptr;
+};
 
 pkv_pruner make_pruner(pkv_ctx ctx, pkv_mapper m, int64_t Hq, int64_t dp, int64_t dt, int64_t N, double rho,
                        uint32_t score_flags, uint32_t mode, int world, int rank, pkv_comm comm) {
@@ -79,7 +96,8 @@ pkv_pruner make_pruner(pkv_ctx ctx, pkv_mapper m, int64_t Hq, int64_t dp, int64_
 // score -> map (-> exchange) on `ps`; select -> compact on `ts` (gated by an
 // event when the streams differ).
 void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, const void* vt, void* k_out,
-                void* v_out, int32_t* idx_out, float* scores_out, cudaStream_t ps, cudaStream_t ts) {
+                void* v_out, int32_t* idx_out, float* scores_out, cudaStream_t ps, cudaStream_t ts,
+                const HostArrival* arr = nullptr) {
     const ScoreShape& s = p->score;
     const ShardPlan& pl = p->plan;
     const int64_t slices = p->slices();
@@ -97,9 +115,25 @@ void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, con
         const auto* kpp = static_cast<const uint8_t*>(kp) + k_off;
         auto* lam = static_cast<__nv_bfloat16*>(p->lam.get(static_cast<size_t>(s.L * s.Hq * s.Nq) * 16));
         auto* x = static_cast<float*>(p->x.get(static_cast<size_t>(s.L * s.Hkv * s.Nk) * 4));
-        launch_score_lse(s, qp, kpp, nullptr, lam, ps);
-        launch_score_pool(s, qp, kpp, lam, p->reduce_max, x, ps);
-        count_launch(p->ctx, 2);
+        if (!arr) {
+            launch_score_lse(s, qp, kpp, nullptr, lam, ps);
+            launch_score_pool(s, qp, kpp, lam, p->reduce_max, x, ps);
+            count_launch(p->ctx, 2);
+        } else {  // proxy layers scored chunk by chunk as their H2D copies land
+            for (int c = 0; c < arr->chunks; ++c) {
+                const int64_t l0 = c * arr->chunk_layers, l1 = std::min<int64_t>(s.L, l0 + arr->chunk_layers);
+                if (l0 >= l1) break;
+                ScoreShape sc = s;
+                sc.L = l1 - l0;
+                PKV_CUDA(cudaStreamWaitEvent(ps, arr->ev_chunk[c], 0));
+                const auto* qc = qp + static_cast<size_t>(l0 * p->Hq * p->N * p->dp) * 2;
+                const auto* kc = kpp + static_cast<size_t>(l0 * s.Hkv * p->N * p->dp) * 2;
+                __nv_bfloat16* lc = lam + static_cast<size_t>(l0 * s.Hq * s.Nq) * 8;
+                launch_score_lse(sc, qc, kc, nullptr, lc, ps);
+                launch_score_pool(sc, qc, kc, lc, p->reduce_max, x + static_cast<size_t>(l0 * s.Hkv * s.Nk), ps);
+                count_launch(p->ctx, 2);
+            }
+        }
         // (2) mapper: Ŷ for target layers [a, b), all heads
         p->mapper->run(x, p->unit_off, p->N, p->out_unit, y_map, ps);
     }
@@ -111,6 +145,7 @@ void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, con
         PKV_CUDA(cudaStreamWaitEvent(ts, p->ev, 0));
     }
     if (slices == 0) return;
+    if (arr) PKV_CUDA(cudaStreamWaitEvent(ts, arr->ev_kv, 0));
     // (3) Top-K per (target layer, head): ascending retained indices
     launch_topk_select(y_sel, slices, p->N, p->K, nullptr, idx, ts);
     // (4) packed KV gather
@@ -162,21 +197,50 @@ pkv_status pkv_pruner_run_host(pkv_pruner p, const void* q_h, const void* kp_h, 
     return guard([&] {
         PKV_REQUIRE_VALUE(p != nullptr, "null pkv_pruner");
         auto st = static_cast<cudaStream_t>(stream);
+        const ShardPlan& pl = p->plan;
         const int64_t Ls = p->mapper->geom.proxy_layers, Hs = p->mapper->geom.proxy_heads;
-        const size_t qb = static_cast<size_t>(Ls * p->Hq * p->N * p->dp) * 2;
-        const size_t kpb = static_cast<size_t>(Ls * Hs * p->N * p->dp) * 2;
+        const size_t q_layer = static_cast<size_t>(p->Hq * p->N * p->dp) * 2;
+        const size_t kp_layer = static_cast<size_t>(Hs * p->N * p->dp) * 2;
+        const size_t qb = Ls * q_layer, kpb = Ls * kp_layer;
         const size_t kvb = static_cast<size_t>(p->slices() * p->N * p->dt) * 2;
         const size_t ob = static_cast<size_t>(p->slices() * p->K * p->dt) * 2;
         const size_t ib = static_cast<size_t>(p->slices() * p->K) * 4;
         auto* in = static_cast<uint8_t*>(p->host_in.get(qb + kpb + 2 * kvb));
         auto* outb = static_cast<uint8_t*>(p->host_out.get(2 * ob + ib));
-        PKV_CUDA(cudaMemcpyAsync(in, q_h, qb, cudaMemcpyHostToDevice, st));
-        PKV_CUDA(cudaMemcpyAsync(in + qb, kp_h, kpb, cudaMemcpyHostToDevice, st));
-        PKV_CUDA(cudaMemcpyAsync(in + qb + kpb, kt_h, kvb, cudaMemcpyHostToDevice, st));
-        PKV_CUDA(cudaMemcpyAsync(in + qb + kpb + kvb, vt_h, kvb, cudaMemcpyHostToDevice, st));
-        const pkv_status rc = pkv_pruner_run(p, in, in + qb, in + qb + kpb, in + qb + kpb + kvb, outb, outb + ob,
-                                             reinterpret_cast<int32_t*>(outb + 2 * ob), nullptr, stream);
-        if (rc != PKV_OK) throw Error{rc, pkv_last_error()};
+        if (!p->copy_st) {
+            PKV_CUDA(cudaStreamCreateWithFlags(&p->copy_st, cudaStreamNonBlocking));
+            for (cudaEvent_t& e : p->ev_in) PKV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        cudaStream_t cs = p->copy_st;
+        constexpr int kC = pkv_pruner_s::kChunks;
+        // the copies may overwrite the input buffers only after earlier work on `st`
+        PKV_CUDA(cudaEventRecord(p->ev_in[kC + 1], st));
+        PKV_CUDA(cudaStreamWaitEvent(cs, p->ev_in[kC + 1], 0));
+        // H2D overlapped with compute: the proxy layers this pruner scores, in
+        // kC chunks (scoring of chunk c starts when it lands), then the target
+        // KV (needed only by select + compaction, after the mapper)
+        HostArrival arr;
+        const int64_t nl = pl.b > pl.a ? pl.p_hi - pl.p_lo : 0;
+        arr.chunk_layers = std::max<int64_t>(1, (nl + kC - 1) / kC);
+        arr.chunks = kC;
+        arr.ev_chunk = p->ev_in;
+        for (int c = 0; c < kC; ++c) {
+            const int64_t l0 = pl.p_lo + c * arr.chunk_layers;
+            const int64_t l1 = std::min<int64_t>(pl.p_lo + nl, l0 + arr.chunk_layers);
+            if (l0 < l1) {
+                PKV_CUDA(cudaMemcpyAsync(in + l0 * q_layer, static_cast<const uint8_t*>(q_h) + l0 * q_layer,
+                                         (l1 - l0) * q_layer, cudaMemcpyHostToDevice, cs));
+                PKV_CUDA(cudaMemcpyAsync(in + qb + l0 * kp_layer, static_cast<const uint8_t*>(kp_h) + l0 * kp_layer,
+                                         (l1 - l0) * kp_layer, cudaMemcpyHostToDevice, cs));
+            }
+            PKV_CUDA(cudaEventRecord(p->ev_in[c], cs));
+        }
+        PKV_CUDA(cudaMemcpyAsync(in + qb + kpb, kt_h, kvb, cudaMemcpyHostToDevice, cs));
+        PKV_CUDA(cudaMemcpyAsync(in + qb + kpb + kvb, vt_h, kvb, cudaMemcpyHostToDevice, cs));
+        PKV_CUDA(cudaEventRecord(p->ev_in[kC], cs));
+        arr.ev_kv = p->ev_in[kC];
+        run_pruner(p, in, in + qb, in + qb + kpb, in + qb + kpb + kvb, outb, outb + ob,
+                   reinterpret_cast<int32_t*>(outb + 2 * ob), nullptr, st, st, &arr);
         PKV_CUDA(cudaMemcpyAsync(k_out_h, outb, ob, cudaMemcpyDeviceToHost, st));
         PKV_CUDA(cudaMemcpyAsync(v_out_h, outb + ob, ob, cudaMemcpyDeviceToHost, st));
         if (idx_out_h) PKV_CUDA(cudaMemcpyAsync(idx_out_h, outb + 2 * ob, ib, cudaMemcpyDeviceToHost, st));
