@@ -264,6 +264,14 @@ def stage_breakdown(P, ctx, mapper, c, q, kp, kt, vt, ko, vo, K, stream, args):
     out["compact_ms"] = time_loop(
         lambda: P.compact_kv(kt.view(S, c["N"], c["dt"]), vt.view(S, c["N"], c["dt"]), idx, ctx=ctx, stream=stream,
                              out=(ko.view(S, K, c["dt"]), vo.view(S, K, c["dt"]))), it, stream)
+    # causal scoring with the LSE emitted by the proxy's own prefill
+    # attention (its O is the proxy model's output anyway): one scoring pass
+    vp = torch.randn_like(kp)
+    _, plse = P.proxy_prefill_attention(q, kp, vp, causal=True, want_out=True, ctx=ctx)
+    out["x_prefill_attn_causal_ms"] = time_loop(
+        lambda: P.proxy_prefill_attention(q, kp, vp, causal=True, want_out=True, ctx=ctx, stream=stream), it, stream)
+    out["x_score_pool_causal_ms"] = time_loop(
+        lambda: P.score(q, kp, lse=plse, causal=True, ctx=ctx, stream=stream, out=x), it, stream)
     return out
 
 
@@ -448,7 +456,14 @@ def main():
             roof["traffic"] = json.load(open(prof)).get(roof["kernel"])
         sc_b = bytes_select(c) + bytes_compact(c)
         sc_ms = st["select_ms"] + st["compact_ms"]
-        line["stages_ms"] = {k[:-3]: v for k, v in st.items()}
+        line["stages_ms"] = {k[:-3]: v for k, v in st.items() if not k.startswith("x_")}
+        fc = 2 * c["dp"] * (c["N"] * (c["N"] + 1) // 2) * c["Hq"] * c["Ls"]  # causal pairs
+        line["scoring_single_pass"] = {
+            "note": "causal scoring with the LSE from the proxy's prefill attention (pkv_proxy_prefill_attention, "
+                    "SURVEY 8(f)-1): one tensor-core pass; the prefill attention itself is proxy-model work",
+            "proxy_prefill_attn_ms": st["x_prefill_attn_causal_ms"], "score_pool_ms": st["x_score_pool_causal_ms"],
+            "TFLOP/s": fc / st["x_score_pool_causal_ms"] / 1e9,
+            "frac_of_burst": fc / st["x_score_pool_causal_ms"] / 1e9 / tf_burst}
         line["stage_roofline"] = {
             "score_lse": {"TFLOP/s": flops_score_pass(c) / st["score_lse_ms"] / 1e9},
             "score_pool": {"TFLOP/s": flops_score_pass(c) / st["score_pool_ms"] / 1e9},

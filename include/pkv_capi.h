@@ -105,6 +105,17 @@ pkv_status pkv_score(pkv_ctx ctx, const void* q_dev, const void* k_dev, int64_t 
 pkv_status pkv_score_lse(pkv_ctx ctx, const void* q_dev, const void* k_dev, int64_t L, int64_t Hq, int64_t Hkv,
                          int64_t Nq, int64_t Nk, int64_t d, uint32_t flags, float* lse_out_dev, void* stream);
 
+/* Proxy prefill attention that also emits the row LSE (
+ * the scores are a by-product of the proxy's own prefill):
+ *   o_out[l,h,q,:] = softmax(Q·K^T/sqrt(d)) · V   (bf16, nullable)
+ *   lse_out[l,h,q] = log sum_j exp(Q·K_j/sqrt(d))  (fp32, nullable)
+ * q bf16 [L, Hq, Nq, d], k/v bf16 [L, Hkv, Nk, d]; flags: PKV_SCORE_CAUSAL.
+ * Passing lse_out to pkv_score(..., lse_dev = lse_out, ...) makes scoring a
+ * single tensor-core pass. d must be 64 or 128. */
+pkv_status pkv_proxy_prefill_attention(pkv_ctx ctx, const void* q_dev, const void* k_dev, const void* v_dev,
+                                       int64_t L, int64_t Hq, int64_t Hkv, int64_t Nq, int64_t Nk, int64_t d,
+                                       uint32_t flags, void* o_out_dev, float* lse_out_dev, void* stream);
+
 /* ------------------------------------------------------- mapper (a-2) ---- */
 /* geom5 = {target_layers, target_heads, proxy_layers, proxy_heads, head_dim}
  *   (ModelGeometry, proj/include/proxykv/mapper.hpp:16-25)

@@ -63,6 +63,8 @@ SIGNATURES = {
                                       _c_vp, _c_vp]),
     "pkv_score": (ctypes.c_int, [_c_vp, _c_vp, _c_vp] + [_c_i64] * 6 + [_c_u32, _c_vp, _c_vp, _c_vp]),
     "pkv_score_lse": (ctypes.c_int, [_c_vp, _c_vp, _c_vp] + [_c_i64] * 6 + [_c_u32, _c_vp, _c_vp]),
+    "pkv_proxy_prefill_attention": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp] + [_c_i64] * 6 + [_c_u32, _c_vp, _c_vp,
+                                                                                              _c_vp]),
     "pkv_layer_pair": (ctypes.c_int, [_c_i64, _c_i64p, _c_i64p]),
     "pkv_window_offsets": (ctypes.c_int, [_c_i64, _c_i64, _c_i64, _c_i64p, _c_i64, _c_i64p]),
     "pkv_mapper_init_params": (ctypes.c_int, [_c_i64p, _c_i64p, ctypes.c_uint64, _c_vp, _c_i64p]),

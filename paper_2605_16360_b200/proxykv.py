@@ -22,6 +22,7 @@ from ._lib import ConfigError, CudaError, NoDeviceError, PkvError, PkvValueError
 __all__ = [
     "Context", "PruneMask", "MaskApplication", "ModelGeometry", "MapperConfig", "Mapper", "Pruner",
     "retention_count", "topk_select", "topk_mask", "apply_mask", "compact_kv", "score", "score_lse",
+    "proxy_prefill_attention",
     "layer_pair", "window_offsets", "mapper_init_params", "ShapeError", "PkvValueError", "ConfigError",
     "CudaError", "NoDeviceError", "PkvError", "SCORE_REDUCE_MAX", "SCORE_REDUCE_SUM", "SCORE_CAUSAL",
     "MAPPER_FP16", "MAPPER_FP16X2", "MAPPER_FP16X3", "SHARD_LAYER", "SHARD_HEAD", "ShardPlan", "shard_plan",
@@ -187,6 +188,21 @@ def score(q, k, *, reduce: str = "max", causal: bool = False, lse=None, ctx: Con
     check(lib().pkv_score(ctx.h, _ptr(q), _ptr(k), L, hq, hkv, nq, nk, d, flags, _ptr(lse), _ptr(x),
                           _stream(stream)))
     return x
+
+
+def proxy_prefill_attention(q, k, v, *, causal: bool = True, want_out: bool = True, ctx: Context = None,
+                            stream=None):
+    """Proxy prefill attention (bf16): returns (O bf16 [L, Hq, Nq, d] | None, lse fp32 [L, Hq, Nq]); the LSE is
+    what `score(..., lse=...)` takes to skip its first pass."""
+    torch = _torch()
+    ctx = ctx or Context.default(q.device.index or 0)
+    L, hq, nq, d = q.shape
+    _, hkv, nk, _ = k.shape
+    o = torch.empty_like(q) if want_out else None
+    lse = torch.empty((L, hq, nq), dtype=torch.float32, device=q.device)
+    check(lib().pkv_proxy_prefill_attention(ctx.h, _ptr(q), _ptr(k), _ptr(v), L, hq, hkv, nq, nk, d,
+                                            SCORE_CAUSAL if causal else 0, _ptr(o), _ptr(lse), _stream(stream)))
+    return o, lse
 
 
 def score_lse(q, k, *, causal: bool = False, ctx: Context = None, stream=None):
