@@ -193,6 +193,16 @@ pkv_status pkv_pruner_run_dual(pkv_pruner p, const void* q_dev, const void* kp_d
                                const void* vt_dev, void* k_out_dev, void* v_out_dev, int32_t* idx_out_dev,
                                float* scores_out_dev, void* proxy_stream, void* target_stream);
 
+/* Target-side consumption of the packed cache: one
+ * decode query per query head over its KV head's retained rows,
+ *   out[l,h,:] = softmax(q[l,h]·K_packed[l,h/g]^T · scale) · V_packed[l,h/g]
+ * q bf16 [L, Hq, d] (L: layers or independent sequences), k/v_packed bf16
+ * [L, Hkv, K, d] as written by pkv_compact_kv / pkv_pruner_run, out fp32
+ * [L, Hq, d]. Split-K flash decoding, HBM-bound; GQA groups 1/2/4/8, d 64/128. */
+pkv_status pkv_packed_decode_attention(pkv_ctx ctx, const void* q_dev, const void* k_packed_dev,
+                                       const void* v_packed_dev, int64_t L, int64_t Hq, int64_t Hkv, int64_t K,
+                                       int64_t d, double scale, float* out_dev, void* stream);
+
 /* ------------------------------------------------ multi-GPU -- */
 /* One context pruned by `world` ranks (one process per GPU). No reference
  * code: the reference is single-threaded CPU; BASELINE.json configs[2,3].

@@ -79,6 +79,8 @@ SIGNATURES = {
     "pkv_pruner_run": (ctypes.c_int, [_c_vp] * 10),
     "pkv_pruner_run_host": (ctypes.c_int, [_c_vp] * 9),
     "pkv_pruner_run_dual": (ctypes.c_int, [_c_vp] * 11),
+    "pkv_packed_decode_attention": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp] + [_c_i64] * 5 + [_c_dbl, _c_vp,
+                                                                                                _c_vp]),
     "pkv_shard_plan": (ctypes.c_int, [_c_i64p, ctypes.c_int, ctypes.c_int, _c_u32, _c_i64p]),
     "pkv_comm_unique_id": (ctypes.c_int, [_c_vp]),
     "pkv_comm_create": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_vp, ctypes.POINTER(_c_vp)]),

@@ -1,0 +1,272 @@
+// decode.cu — target-side consumption of the packed cache (SURVEY.md §8(f)
+// item 2; the target decodes over the pruned KV): one decode
+// query per query head attends over its KV head's K retained rows,
+//   o[l, h, :] = softmax(q[l, h]·K_packed[l, h/g]ᵀ · scale) · V_packed[l, h/g]
+// bf16 q/K/V, fp32 math and output, GQA group g = Hq / Hkv <= 8, head_dim 128
+// (or 64).
+//
+// HBM-bound (every retained K/V byte is read once; the packed cache is ρ of
+// the full one, so decode time scales with ρ). Split-K flash decoding:
+//   pass 1: CTA = (key split, KV head, layer), 8 warps; a warp handles four
+//     keys per step with 8 lanes per key row (16 dims per lane at d = 128:
+//     32-byte coalesced loads, 1 KB per warp instruction; 16 lanes and two
+//     keys when g = 8, for registers), all g query heads of the
+//     group against each row (K/V read once for the group); each 8-lane group
+//     keeps its own online (max, sum, o) state, so no per-key cross-group
+//     traffic — three shuffle steps finish each dot. States are merged in
+//     shared memory and one partial per (split, head) goes to global.
+//   pass 2: merge the splits (log-sum-exp weighted) into o.
+#include <cuda_bf16.h>
+
+#include "decode.cuh"
+#include "sm100.cuh"
+
+namespace pkv {
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kMaxG = 8;
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        f[2 * i] = __uint_as_float(w[i] << 16);
+        f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+}
+
+using sm100::ex2;
+using sm100::ffma2;
+using sm100::pack2;
+using sm100::unpack2;
+
+// partial: [L, Hq, splits] x {m (log2 domain), l, o[D]}. G: group-size
+// bucket (1, 2, 4, 8); g <= G heads are live (g = 7 for Qwen-2.5-7B).
+template <int D, int G>
+__global__ void __launch_bounds__(32 * kWarps)
+    decode_split_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kc,
+                        const __nv_bfloat16* __restrict__ vc, int Hq, int Hkv, int g, int64_t K, int64_t chunk,
+                        float scale_log2, float* __restrict__ part) {
+    // lanes per key row: 8 (16 dims each at d = 128), 16 for G = 8 at d = 128 (register budget)
+    constexpr int kLPK = (G >= 8 && D == 128) ? 16 : 8;
+    constexpr int kKPW = 32 / kLPK;  // keys per warp step
+    constexpr int kDL = D / kLPK;    // dims per lane
+    const int split = blockIdx.x, kh = blockIdx.y, l = blockIdx.z;
+    const int splits = gridDim.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = lane / kLPK, sub = lane % kLPK;  // key group, lane within the group
+    const int64_t k_lo = split * chunk, k_hi = min(K, k_lo + chunk);
+    const int64_t kslab = (int64_t)l * Hkv + kh;
+    const __nv_bfloat16* kbase = kc + kslab * K * D + sub * kDL;
+    const __nv_bfloat16* vbase = vc + kslab * K * D + sub * kDL;
+
+    // this lane's slice of the group's queries (pre-scaled to the log2 domain)
+    float qr[G][kDL];
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+        const __nv_bfloat16* qp = q + ((int64_t)l * Hq + kh * g + (h < g ? h : 0)) * D + sub * kDL;
+#pragma unroll
+        for (int c = 0; c < kDL; c += 8) {
+            float f[8];
+            bf16x8_to_f32(*reinterpret_cast<const uint4*>(qp + c), f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) qr[h][c + e] = f[e] * scale_log2;
+        }
+    }
+    float m[G], ls[G], o[G][kDL];
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+        m[h] = -INFINITY;
+        ls[h] = 0.0f;
+#pragma unroll
+        for (int e = 0; e < kDL; ++e) o[h][e] = 0.0f;
+    }
+    // keys of this CTA: warp w, group r take key k_lo + kKPW*(w + kWarps*i) + r.
+    // The loop runs warp-uniformly (the dot reductions shuffle across the
+    // warp); a group past the chunk end computes on a clamped row and skips
+    // its state update.
+    // raw 16-byte row slices of the current and the next key (register double
+    // buffer: the next step's loads are in flight during this step's math)
+    constexpr int kV = kDL / 8;
+    uint4 kraw[kV], vraw[kV], knx[kV], vnx[kV];
+    auto load_row = [&](int64_t key0, uint4 (&kr)[kV], uint4 (&vr)[kV]) {
+        const int64_t key = key0 + grp;
+        const int64_t kk = key < k_hi ? key : k_lo;
+#pragma unroll
+        for (int c = 0; c < kV; ++c) {
+            kr[c] = __ldcs(reinterpret_cast<const uint4*>(kbase + kk * D + 8 * c));
+            vr[c] = __ldcs(reinterpret_cast<const uint4*>(vbase + kk * D + 8 * c));
+        }
+    };
+    const int64_t kstep = kKPW * kWarps;
+    if (k_lo + kKPW * warp < k_hi) load_row(k_lo + kKPW * warp, kraw, vraw);
+    for (int64_t key0 = k_lo + kKPW * warp; key0 < k_hi; key0 += kstep) {
+        const int64_t key = key0 + grp;
+        const bool ok = key < k_hi;
+        if (key0 + kstep < k_hi) load_row(key0 + kstep, knx, vnx);
+        float kf[kDL], vf[kDL];
+#pragma unroll
+        for (int c = 0; c < kV; ++c) {
+            float f[8];
+            bf16x8_to_f32(kraw[c], f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) kf[8 * c + e] = f[e];
+            bf16x8_to_f32(vraw[c], f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) vf[8 * c + e] = f[e];
+        }
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            if (h >= g) break;  // warp-uniform
+            // dot as packed FFMA2 over dimension pairs, then the group reduction
+            uint64_t s2 = pack2(0.0f, 0.0f);
+#pragma unroll
+            for (int e = 0; e < kDL; e += 2) s2 = ffma2(pack2(qr[h][e], qr[h][e + 1]), pack2(kf[e], kf[e + 1]), s2);
+            const float2 sp = unpack2(s2);
+            float s = sp.x + sp.y;
+#pragma unroll
+            for (int o2 = 1; o2 < kLPK; o2 <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o2);
+            if (ok) {
+                const float mn = fmaxf(m[h], s);
+                const float a = ex2(m[h] - mn), p = ex2(s - mn);  // ex2(-inf) = 0
+                ls[h] = ls[h] * a + p;
+                const uint64_t aa = pack2(a, a), pp = pack2(p, p);
+#pragma unroll
+                for (int e = 0; e < kDL; e += 2) {
+                    const uint64_t oe = sm100::fmul2(pack2(o[h][e], o[h][e + 1]), aa);
+                    const float2 r = unpack2(ffma2(pp, pack2(vf[e], vf[e + 1]), oe));
+                    o[h][e] = r.x;
+                    o[h][e + 1] = r.y;
+                }
+                m[h] = mn;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < kV; ++c) {
+            kraw[c] = knx[c];
+            vraw[c] = vnx[c];
+        }
+    }
+    // merge the 32 group states per head through shared memory
+    constexpr int kGroupsCta = kWarps * kKPW;
+    __shared__ float s_m[kGroupsCta][G], s_l[kGroupsCta][G];
+    __shared__ float s_o[G][D];
+    const int gid = warp * kKPW + grp;
+    if (sub == 0) {
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            s_m[gid][h] = m[h];
+            s_l[gid][h] = ls[h];
+        }
+    }
+    for (int i = threadIdx.x; i < G * D; i += blockDim.x) s_o[i / D][i % D] = 0.0f;
+    __syncthreads();
+    float M[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+        M[h] = -INFINITY;
+        for (int r = 0; r < kGroupsCta; ++r) M[h] = fmaxf(M[h], s_m[r][h]);
+    }
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+        const float w = M[h] == -INFINITY ? 0.0f : exp2f(m[h] - M[h]);
+#pragma unroll
+        for (int e = 0; e < kDL; ++e) atomicAdd(&s_o[h][sub * kDL + e], o[h][e] * w);
+    }
+    __syncthreads();
+    const int64_t pstride = 2 + D;
+    for (int i = threadIdx.x; i < g * D; i += blockDim.x) {
+        const int h = i / D, e = i % D;
+        float* pp = part + (((int64_t)l * Hq + kh * g + h) * splits + split) * pstride;
+        pp[2 + e] = s_o[h][e];
+        if (e == 0) {
+            float L = 0.0f;
+            for (int r = 0; r < kGroupsCta; ++r)
+                L += s_m[r][h] == -INFINITY ? 0.0f : s_l[r][h] * exp2f(s_m[r][h] - M[h]);
+            pp[0] = M[h];
+            pp[1] = L;
+        }
+    }
+}
+
+template <int D>
+__global__ void decode_merge_kernel(const float* __restrict__ part, int splits, float* __restrict__ out) {
+    const int64_t head = blockIdx.x;  // l * Hq + h
+    const float* pp = part + head * splits * (2 + D);
+    float M = -INFINITY;
+    for (int s = 0; s < splits; ++s) M = fmaxf(M, pp[s * (2 + D)]);
+    float L = 0.0f;
+    for (int s = 0; s < splits; ++s) {
+        const float ms = pp[s * (2 + D)];
+        L += ms == -INFINITY ? 0.0f : pp[s * (2 + D) + 1] * exp2f(ms - M);
+    }
+    for (int e = threadIdx.x; e < D; e += blockDim.x) {
+        float acc = 0.0f;
+        for (int s = 0; s < splits; ++s) {
+            const float ms = pp[s * (2 + D)];
+            if (ms != -INFINITY) acc += pp[s * (2 + D) + 2 + e] * exp2f(ms - M);
+        }
+        out[head * D + e] = L > 0.0f ? acc / L : 0.0f;
+    }
+}
+
+template <int D, int G>
+void run_decode(const DecodeShape& s, const void* q, const void* kc, const void* vc, float* out, DevBuf& ws,
+                int sm_count, cudaStream_t st) {
+    const int64_t heads = s.L * s.Hkv;
+    // ~2 waves of CTAs (more splits cost more in per-CTA setup and the merge
+    // than a partial last wave), at least 64 keys per split
+    int64_t splits = (2 * sm_count + heads - 1) / heads;
+    splits = std::max<int64_t>(1, std::min<int64_t>(splits, (s.K + 63) / 64));
+    const int64_t chunk = (s.K + splits - 1) / splits;
+    splits = (s.K + chunk - 1) / chunk;
+    float* part = static_cast<float*>(ws.get(static_cast<size_t>(s.L * s.Hq * splits * (2 + D)) * 4));
+    const dim3 grid((unsigned)splits, (unsigned)s.Hkv, (unsigned)s.L);
+    decode_split_kernel<D, G><<<grid, 32 * kWarps, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(kc),
+        static_cast<const __nv_bfloat16*>(vc), (int)s.Hq, (int)s.Hkv, (int)(s.Hq / s.Hkv), s.K, chunk,
+        s.scale * 1.4426950408889634f, part);
+    check_launch("decode_split_kernel");
+    decode_merge_kernel<D><<<(unsigned)(s.L * s.Hq), D, 0, st>>>(part, (int)splits, out);
+    check_launch("decode_merge_kernel");
+}
+
+template <int D>
+void dispatch_g(const DecodeShape& s, const void* q, const void* kc, const void* vc, float* out, DevBuf& ws, int sm,
+                cudaStream_t st) {
+    const int64_t g = s.Hq / s.Hkv;
+    if (g <= 1) return run_decode<D, 1>(s, q, kc, vc, out, ws, sm, st);
+    if (g <= 2) return run_decode<D, 2>(s, q, kc, vc, out, ws, sm, st);
+    if (g <= 4) return run_decode<D, 4>(s, q, kc, vc, out, ws, sm, st);
+    return run_decode<D, 8>(s, q, kc, vc, out, ws, sm, st);
+}
+
+}  // namespace
+
+void launch_packed_decode(const DecodeShape& s, const void* q, const void* kc, const void* vc, float* out, DevBuf& ws,
+                          int sm_count, cudaStream_t st) {
+    if (s.d == 128) dispatch_g<128>(s, q, kc, vc, out, ws, sm_count, st);
+    else dispatch_g<64>(s, q, kc, vc, out, ws, sm_count, st);
+}
+
+}  // namespace pkv
+
+using namespace pkv;
+
+extern "C" pkv_status pkv_packed_decode_attention(pkv_ctx ctx, const void* q_dev, const void* k_packed_dev,
+                                                  const void* v_packed_dev, int64_t L, int64_t Hq, int64_t Hkv,
+                                                  int64_t K, int64_t d, double scale, float* out_dev, void* stream) {
+    return guard([&] {
+        require_ctx(ctx);
+        PKV_REQUIRE_SHAPE(L > 0 && Hq > 0 && Hkv > 0 && K > 0, "packed decode extents must be positive");
+        PKV_REQUIRE_SHAPE(Hq % Hkv == 0, "query heads ", Hq, " not a multiple of KV heads ", Hkv);
+        PKV_REQUIRE(d == 64 || d == 128, PKV_ECONFIG, "packed decode supports head_dim 64 or 128, got ", d);
+        PKV_REQUIRE(Hq / Hkv <= kMaxG, PKV_ECONFIG, "packed decode supports GQA groups up to ", kMaxG);
+        PKV_REQUIRE(L * Hkv <= 65535, PKV_ECONFIG, "too many (layer, KV head) pairs for one launch");
+        DecodeShape s{L, Hq, Hkv, K, d, static_cast<float>(scale)};
+        launch_packed_decode(s, q_dev, k_packed_dev, v_packed_dev, out_dev, ctx->scratch_decode, ctx->sm_count,
+                             static_cast<cudaStream_t>(stream));
+        count_launch(ctx, 2);
+    });
+}

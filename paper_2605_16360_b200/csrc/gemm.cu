@@ -106,12 +106,6 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpiParams& p, int64_t r
 // tile so global loads/stores are row-contiguous across the warp (128 B fp32
 // rows, or two 64 B fp16 rows per instruction) instead of 32 scattered
 // per-thread rows (partial-sector traffic).
-__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
-    uint64_t d;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-
 // gelu_fast (sm100.cuh) on a packed pair: the FMA-pipe work as FFMA2/FMUL2.
 __device__ __forceinline__ float2 gelu_fast2(float x0, float x1) {
     const uint64_t z = fmul2(pack2(fabsf(x0), fabsf(x1)), pack2(0.70710678118654752f, 0.70710678118654752f));

@@ -77,6 +77,7 @@ struct pkv_ctx_s {
     pkv::DevBuf scratch_select;
     pkv::DevBuf scratch_host_io;
     pkv::DevBuf scratch_score;
+    pkv::DevBuf scratch_decode;
 };
 
 namespace pkv {

@@ -22,7 +22,7 @@ from ._lib import ConfigError, CudaError, NoDeviceError, PkvError, PkvValueError
 __all__ = [
     "Context", "PruneMask", "MaskApplication", "ModelGeometry", "MapperConfig", "Mapper", "Pruner",
     "retention_count", "topk_select", "topk_mask", "apply_mask", "compact_kv", "score", "score_lse",
-    "proxy_prefill_attention",
+    "proxy_prefill_attention", "packed_decode_attention",
     "layer_pair", "window_offsets", "mapper_init_params", "ShapeError", "PkvValueError", "ConfigError",
     "CudaError", "NoDeviceError", "PkvError", "SCORE_REDUCE_MAX", "SCORE_REDUCE_SUM", "SCORE_CAUSAL",
     "MAPPER_FP16", "MAPPER_FP16X2", "MAPPER_FP16X3", "SHARD_LAYER", "SHARD_HEAD", "ShardPlan", "shard_plan",
@@ -203,6 +203,20 @@ def proxy_prefill_attention(q, k, v, *, causal: bool = True, want_out: bool = Tr
     check(lib().pkv_proxy_prefill_attention(ctx.h, _ptr(q), _ptr(k), _ptr(v), L, hq, hkv, nq, nk, d,
                                             SCORE_CAUSAL if causal else 0, _ptr(o), _ptr(lse), _stream(stream)))
     return o, lse
+
+
+def packed_decode_attention(q, k_packed, v_packed, *, scale: float = None, ctx: Context = None, stream=None,
+                            out=None):
+    """Decode over the packed cache: q bf16 [L, Hq, d], k/v_packed bf16 [L, Hkv, K, d] -> fp32 [L, Hq, d]."""
+    torch = _torch()
+    ctx = ctx or Context.default(q.device.index or 0)
+    L, hq, d = q.shape
+    _, hkv, K, _ = k_packed.shape
+    o = out if out is not None else torch.empty((L, hq, d), dtype=torch.float32, device=q.device)
+    sc = float(scale) if scale is not None else 1.0 / d ** 0.5
+    check(lib().pkv_packed_decode_attention(ctx.h, _ptr(q), _ptr(k_packed), _ptr(v_packed), L, hq, hkv, K, d, sc,
+                                            _ptr(o), _stream(stream)))
+    return o
 
 
 def score_lse(q, k, *, causal: bool = False, ctx: Context = None, stream=None):
