@@ -38,7 +38,12 @@ typedef enum {
     PKV_ECUDA = 3,   /* CUDA runtime / launch failure */
     PKV_ENCCL = 4,   /* reserved: collective failure */
     PKV_ECONFIG = 5, /* ConfigError (incl. configurations the GPU path does not support) */
-    PKV_ENODEV = 6   /* no sm_100 device */
+    PKV_ENODEV = 6,  /* no sm_100 device */
+    PKV_EIO = 7,           /* IoError (common.hpp:33) */
+    PKV_EIO_MAGIC = 8,     /* BadMagicError */
+    PKV_EIO_VERSION = 9,   /* VersionMismatchError */
+    PKV_EIO_TRUNCATED = 10, /* TruncatedFileError */
+    PKV_EIO_LENGTH = 11    /* PayloadLengthError */
 } pkv_status;
 
 typedef struct pkv_ctx_s* pkv_ctx;
@@ -202,6 +207,25 @@ pkv_status pkv_pruner_run_dual(pkv_pruner p, const void* q_dev, const void* kp_d
 pkv_status pkv_packed_decode_attention(pkv_ctx ctx, const void* q_dev, const void* k_packed_dev,
                                        const void* v_packed_dev, int64_t L, int64_t Hq, int64_t Hkv, int64_t K,
                                        int64_t d, double scale, float* out_dev, void* stream);
+
+/* ------------------------------------------- file formats -- */
+/* Host-only. Little-endian, binio.hpp semantics; corrupt files return the
+ * PKV_EIO_* code of the reference's IoError taxonomy (common.hpp:33-52).
+ * PKVT trace: geom6 = {L_s, H_s, L_l, H_l, N, B};
+ * per sample X fp32 [B, L_s, H_s, N] then Y fp32 [B, L_l, H_l, N]; meta is a
+ * free one-line string (nullable). read(write(t)) is bit-exact. */
+pkv_status pkv_trace_write(const char* path, const int64_t* geom6, int64_t samples, const float* x, const float* y,
+                           const char* meta);
+pkv_status pkv_trace_read_header(const char* path, int64_t* geom6_out, int64_t* samples_out);
+/* x_out / y_out hold samples * [B, L, H, N] floats (sizes from the header). */
+pkv_status pkv_trace_read(const char* path, float* x_out, float* y_out);
+/* Mapper checkpoint: geometry, config, tensor directory and the
+ * fp64 parameter blob in the pkv_mapper_init_params / pkv_mapper_create
+ * layout. blob_out may be NULL to query count_out. */
+pkv_status pkv_checkpoint_write(const char* path, const int64_t* geom5, const int64_t* cfg12, const double* blob,
+                                int64_t count);
+pkv_status pkv_checkpoint_read(const char* path, int64_t* geom5_out, int64_t* cfg12_out, double* blob_out,
+                               int64_t* count_out);
 
 /* ------------------------------------------------ multi-GPU -- */
 /* One context pruned by `world` ranks (one process per GPU). No reference

@@ -36,6 +36,22 @@ struct CudaError : Error {
 struct NoDeviceError : Error {
     using Error::Error;
 };
+// common.hpp:33-52: the corrupted-file taxonomy of the trace / checkpoint formats
+struct IoError : Error {
+    using Error::Error;
+};
+struct BadMagicError : IoError {
+    using IoError::IoError;
+};
+struct VersionMismatchError : IoError {
+    using IoError::IoError;
+};
+struct TruncatedFileError : IoError {
+    using IoError::IoError;
+};
+struct PayloadLengthError : IoError {
+    using IoError::IoError;
+};
 
 inline void check(pkv_status s) {
     if (s == PKV_OK) return;
@@ -45,6 +61,11 @@ inline void check(pkv_status s) {
         case PKV_EVALUE: throw ValueError(msg);
         case PKV_ECONFIG: throw ConfigError(msg);
         case PKV_ENODEV: throw NoDeviceError(msg);
+        case PKV_EIO: throw IoError(msg);
+        case PKV_EIO_MAGIC: throw BadMagicError(msg);
+        case PKV_EIO_VERSION: throw VersionMismatchError(msg);
+        case PKV_EIO_TRUNCATED: throw TruncatedFileError(msg);
+        case PKV_EIO_LENGTH: throw PayloadLengthError(msg);
         default: throw CudaError(msg);
     }
 }

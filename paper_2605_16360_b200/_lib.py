@@ -40,7 +40,28 @@ class NoDeviceError(PkvError):
     """No sm_100 device: the B200 path has no CPU fallback."""
 
 
-_STATUS = {1: ShapeError, 2: PkvValueError, 3: CudaError, 4: CudaError, 5: ConfigError, 6: NoDeviceError}
+class IoError(PkvError):
+    """proxykv::IoError (common.hpp:33)."""
+
+
+class BadMagicError(IoError):
+    """proxykv::BadMagicError (common.hpp:38)."""
+
+
+class VersionMismatchError(IoError):
+    """proxykv::VersionMismatchError (common.hpp:42)."""
+
+
+class TruncatedFileError(IoError):
+    """proxykv::TruncatedFileError (common.hpp:46)."""
+
+
+class PayloadLengthError(IoError):
+    """proxykv::PayloadLengthError (common.hpp:50)."""
+
+
+_STATUS = {1: ShapeError, 2: PkvValueError, 3: CudaError, 4: CudaError, 5: ConfigError, 6: NoDeviceError, 7: IoError,
+           8: BadMagicError, 9: VersionMismatchError, 10: TruncatedFileError, 11: PayloadLengthError}
 
 _c_i64 = ctypes.c_int64
 _c_i64p = ctypes.POINTER(ctypes.c_int64)
@@ -82,6 +103,11 @@ SIGNATURES = {
     "pkv_packed_decode_attention": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp] + [_c_i64] * 5 + [_c_dbl, _c_vp,
                                                                                                 _c_vp]),
     "pkv_shard_plan": (ctypes.c_int, [_c_i64p, ctypes.c_int, ctypes.c_int, _c_u32, _c_i64p]),
+    "pkv_trace_write": (ctypes.c_int, [ctypes.c_char_p, _c_i64p, _c_i64, _c_vp, _c_vp, ctypes.c_char_p]),
+    "pkv_trace_read_header": (ctypes.c_int, [ctypes.c_char_p, _c_i64p, _c_i64p]),
+    "pkv_trace_read": (ctypes.c_int, [ctypes.c_char_p, _c_vp, _c_vp]),
+    "pkv_checkpoint_write": (ctypes.c_int, [ctypes.c_char_p, _c_i64p, _c_i64p, _c_vp, _c_i64]),
+    "pkv_checkpoint_read": (ctypes.c_int, [ctypes.c_char_p, _c_i64p, _c_i64p, _c_vp, _c_i64p]),
     "pkv_comm_unique_id": (ctypes.c_int, [_c_vp]),
     "pkv_comm_create": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_vp, ctypes.POINTER(_c_vp)]),
     "pkv_comm_destroy": (None, [_c_vp]),

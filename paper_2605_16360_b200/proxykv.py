@@ -17,7 +17,8 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _lib
-from ._lib import ConfigError, CudaError, NoDeviceError, PkvError, PkvValueError, ShapeError, check, lib
+from ._lib import (BadMagicError, ConfigError, CudaError, IoError, NoDeviceError, PayloadLengthError, PkvError,
+                   PkvValueError, ShapeError, TruncatedFileError, VersionMismatchError, check, lib)
 
 __all__ = [
     "Context", "PruneMask", "MaskApplication", "ModelGeometry", "MapperConfig", "Mapper", "Pruner",
@@ -26,7 +27,8 @@ __all__ = [
     "layer_pair", "window_offsets", "mapper_init_params", "ShapeError", "PkvValueError", "ConfigError",
     "CudaError", "NoDeviceError", "PkvError", "SCORE_REDUCE_MAX", "SCORE_REDUCE_SUM", "SCORE_CAUSAL",
     "MAPPER_FP16", "MAPPER_FP16X2", "MAPPER_FP16X3", "SHARD_LAYER", "SHARD_HEAD", "ShardPlan", "shard_plan",
-    "Comm",
+    "Comm", "write_trace", "read_trace", "write_checkpoint", "read_checkpoint", "IoError", "BadMagicError",
+    "VersionMismatchError", "TruncatedFileError", "PayloadLengthError",
 ]
 
 SCORE_REDUCE_MAX = 0
@@ -301,7 +303,7 @@ class Mapper:
     """Device-resident HybridAxialMapper (pkv_mapper)."""
 
     def __init__(self, geom: ModelGeometry, cfg: MapperConfig, blob: np.ndarray = None, *, seed: int = 0,
-                 precision: int = MAPPER_FP16X2, ctx: Context = None):
+                 precision: int = MAPPER_FP16X3, ctx: Context = None):
         self.geom, self.cfg = geom, cfg
         self.ctx = ctx or Context.default()
         if blob is None:
@@ -311,6 +313,12 @@ class Mapper:
         check(lib().pkv_mapper_create(self.ctx.h, geom.as5(), cfg.as12(), blob.ctypes.data, blob.size,
                                       precision, ctypes.byref(h)))
         self.h = h
+
+    @classmethod
+    def from_checkpoint(cls, path: str, *, precision: int = MAPPER_FP16X3, ctx: "Context" = None) -> "Mapper":
+        """A trained mapper (SPEC.md:198 checkpoint) on the device."""
+        geom, cfg, blob = read_checkpoint(path)
+        return cls(geom, cfg, blob, precision=precision, ctx=ctx)
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -435,3 +443,46 @@ class Pruner:
         """Host (ideally pinned) torch tensors in and out; copies happen inside the call."""
         check(lib().pkv_pruner_run_host(self.h, _ptr(q), _ptr(kp), _ptr(kt), _ptr(vt), _ptr(k_out), _ptr(v_out),
                                         _ptr(idx_out), _stream(stream)))
+
+
+# ------------------------------------------------------------ file formats --
+def write_trace(path: str, x: np.ndarray, y: np.ndarray, meta: str = "") -> None:
+    """PKVT trace: x fp32 [S, B, L_s, H_s, N], y fp32 [S, B, L_l, H_l, N]."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    y = np.ascontiguousarray(y, dtype=np.float32)
+    if x.ndim != 5 or y.ndim != 5 or x.shape[0] != y.shape[0] or x.shape[1] != y.shape[1] or x.shape[4] != y.shape[4]:
+        raise ShapeError(f"trace expects x [S,B,L_s,H_s,N] and y [S,B,L_l,H_l,N], got {x.shape} and {y.shape}")
+    S, B, Ls, Hs, N = x.shape
+    g = (ctypes.c_int64 * 6)(Ls, Hs, y.shape[2], y.shape[3], N, B)
+    check(lib().pkv_trace_write(path.encode(), g, S, x.ctypes.data, y.ctypes.data, meta.encode()))
+
+
+def read_trace(path: str) -> Tuple[np.ndarray, np.ndarray]:
+    g = (ctypes.c_int64 * 6)()
+    n = ctypes.c_int64()
+    check(lib().pkv_trace_read_header(path.encode(), g, ctypes.byref(n)))
+    Ls, Hs, Ll, Hl, N, B = (int(v) for v in g)
+    x = np.empty((n.value, B, Ls, Hs, N), np.float32)
+    y = np.empty((n.value, B, Ll, Hl, N), np.float32)
+    check(lib().pkv_trace_read(path.encode(), x.ctypes.data, y.ctypes.data))
+    return x, y
+
+
+def write_checkpoint(path: str, geom: ModelGeometry, cfg: MapperConfig, blob: np.ndarray) -> None:
+    """Mapper checkpoint of a pkv_mapper_init_params-layout fp64 blob."""
+    b = np.ascontiguousarray(blob, dtype=np.float64)
+    check(lib().pkv_checkpoint_write(path.encode(), geom.as5(), cfg.as12(), b.ctypes.data, b.size))
+
+
+def read_checkpoint(path: str) -> Tuple[ModelGeometry, MapperConfig, np.ndarray]:
+    g = (ctypes.c_int64 * 5)()
+    c = (ctypes.c_int64 * 12)()
+    n = ctypes.c_int64()
+    check(lib().pkv_checkpoint_read(path.encode(), g, c, None, ctypes.byref(n)))
+    blob = np.empty(n.value, np.float64)
+    check(lib().pkv_checkpoint_read(path.encode(), g, c, blob.ctypes.data, ctypes.byref(n)))
+    modes = ("active", "bypass")
+    cfg = MapperConfig(d_time=c[0], encoder_layers=c[1], encoder_heads=c[2], ffn_mult=c[3], d_head=c[4],
+                       crop_len=c[5], stride=c[6], synthetic_heads=c[7], stage_conv=modes[c[8]],
+                       stage_encoder=modes[c[9]], stage_cross=modes[c[10]], normalize_input=bool(c[11]))
+    return ModelGeometry(*[int(v) for v in g]), cfg, blob
