@@ -80,6 +80,15 @@ pkv_status pkv_topk_select(pkv_ctx ctx, const float* scores_dev, int64_t slices,
 pkv_status pkv_topk_mask_host(pkv_ctx ctx, const double* scores_host, int64_t slices, int64_t n, double rho,
                               uint8_t* bits_host, int64_t* k_out);
 
+/* Ranking metrics on the device, per slice, fp64:
+ * replaces topk_overlap_per_slice (pruning.cpp:91-108: |a ∩ b| / k) and
+ * captured_mass_per_slice (pruning.cpp:58-80: sum of y over the predicted mask
+ * / sum of y over y's own Top-K, 1 when that is 0). Masks u8 [slices, n]. */
+pkv_status pkv_topk_overlap(pkv_ctx ctx, const uint8_t* mask_a_dev, const uint8_t* mask_b_dev, int64_t slices,
+                            int64_t n, int64_t k, double* per_slice_out_dev, void* stream);
+pkv_status pkv_captured_mass(pkv_ctx ctx, const uint8_t* mask_pred_dev, const float* y_dev, int64_t slices,
+                             int64_t n, int64_t k, double* per_slice_out_dev, void* stream);
+
 /* --------------------------------------------------- compaction (a-4) ---- */
 /* Packed KV gather in apply_mask order (no reference code; the reference only
  * reports indices, pruning.cpp:197-215): for s < slices, j < k,

@@ -516,6 +516,17 @@ class RefLib:
                                             ctypes.byref(k)))
         return bits, k.value
 
+    def captured_mass_per_slice(self, pred_bits: np.ndarray, k: int, y: np.ndarray) -> np.ndarray:
+        """The reference's captured_mass_per_slice (pruning.cpp:58-80)."""
+        yy = np.ascontiguousarray(y, np.float64)
+        pb = np.ascontiguousarray(pred_bits, np.uint8)
+        shape = np.array(yy.shape, np.int64)
+        out = np.zeros(yy.size // yy.shape[-1], np.float64)
+        self.L.pkvref_captured_mass_per_slice.argtypes = [_u8p, ctypes.c_int64, _f64p, _i64p, ctypes.c_int, _f64p]
+        self._check(self.L.pkvref_captured_mass_per_slice(_ptr(pb, _u8p), k, _ptr(yy, _f64p), _ptr(shape, _i64p),
+                                                          yy.ndim, _ptr(out, _f64p)))
+        return out
+
     def apply_mask(self, bits: np.ndarray, k: int, head_dim: int, bytes_per_elem: int = 2):
         b = np.ascontiguousarray(bits, np.uint8)
         shape = np.array(b.shape, np.int64)

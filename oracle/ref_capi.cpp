@@ -123,6 +123,19 @@ int pkvref_topk_overlap_per_slice(const uint8_t* a, const uint8_t* b, const int6
 }
 
 // mapper.cpp:44-49
+// captured_mass_per_slice (pruning.cpp:58-80) over a predicted mask and fp64 scores
+int pkvref_captured_mass_per_slice(const uint8_t* pred, int64_t k, const double* y, const int64_t* shape, int rank,
+                                   double* out) {
+    return guard([&] {
+        PruneMask m;
+        m.shape = Shape(shape, shape + rank);
+        m.bits.assign(pred, pred + shape_numel(m.shape));
+        m.k = k;
+        const auto v = captured_mass_per_slice(m, make_tensor(y, shape, rank));
+        std::memcpy(out, v.data(), v.size() * sizeof(double));
+    });
+}
+
 int pkvref_layer_pair(int64_t target_layer, const int64_t* geom5, int64_t* out) {
     return guard([&] {
         ModelGeometry g{geom5[0], geom5[1], geom5[2], geom5[3], geom5[4]};

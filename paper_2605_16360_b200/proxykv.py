@@ -23,7 +23,7 @@ from ._lib import (BadMagicError, ConfigError, CudaError, IoError, NoDeviceError
 __all__ = [
     "Context", "PruneMask", "MaskApplication", "ModelGeometry", "MapperConfig", "Mapper", "Pruner",
     "retention_count", "topk_select", "topk_mask", "apply_mask", "compact_kv", "score", "score_lse",
-    "proxy_prefill_attention", "packed_decode_attention",
+    "proxy_prefill_attention", "packed_decode_attention", "topk_overlap_device", "captured_mass_device",
     "layer_pair", "window_offsets", "mapper_init_params", "ShapeError", "PkvValueError", "ConfigError",
     "CudaError", "NoDeviceError", "PkvError", "SCORE_REDUCE_MAX", "SCORE_REDUCE_SUM", "SCORE_CAUSAL",
     "MAPPER_FP16", "MAPPER_FP16X2", "MAPPER_FP16X3", "SHARD_LAYER", "SHARD_HEAD", "ShardPlan", "shard_plan",
@@ -160,6 +160,30 @@ def apply_mask(mask: PruneMask, head_dim: int, bytes_per_elem: int = 2) -> MaskA
     app.bytes_saved_per_head = app.dropped_per_slice * head_dim * bytes_per_elem * 2
     app.bytes_saved_total = app.bytes_saved_per_head * slices
     return app
+
+
+def topk_overlap_device(mask_a, mask_b, k: int, *, ctx: Context = None, stream=None):
+    """pruning.cpp:91-108 on the device: per-slice |a ∩ b| / k (fp64 cuda tensor)."""
+    torch = _torch()
+    ctx = ctx or Context.default(mask_a.device.index or 0)
+    n = mask_a.shape[-1]
+    slices = mask_a.numel() // n
+    out = torch.empty(slices, dtype=torch.float64, device=mask_a.device)
+    check(lib().pkv_topk_overlap(ctx.h, _ptr(mask_a.contiguous()), _ptr(mask_b.contiguous()), slices, n, int(k),
+                                 _ptr(out), _stream(stream)))
+    return out
+
+
+def captured_mass_device(mask_pred, y, k: int, *, ctx: Context = None, stream=None):
+    """pruning.cpp:58-80 on the device: per-slice captured-mass ratio (fp64 cuda tensor)."""
+    torch = _torch()
+    ctx = ctx or Context.default(y.device.index or 0)
+    n = y.shape[-1]
+    slices = y.numel() // n
+    out = torch.empty(slices, dtype=torch.float64, device=y.device)
+    check(lib().pkv_captured_mass(ctx.h, _ptr(mask_pred.contiguous()), _ptr(y.contiguous()), slices, n, int(k),
+                                  _ptr(out), _stream(stream)))
+    return out
 
 
 def compact_kv(k_in, v_in, idx_asc, *, ctx: Context = None, stream=None, out=None):
