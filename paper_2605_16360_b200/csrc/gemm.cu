@@ -572,22 +572,32 @@ void dispatch_planes(const GemmArgs& g, int sm, cudaStream_t st) {
 // CTA's TMEM receives its 128 accumulator rows x 256 columns. Per-SM operand
 // traffic drops by a third vs the 128x256 single-CTA tile, which lets the
 // 4-plane FP16X3 stages fit 3-deep.
-template <int NA, int NB>
+// pair kernel epilogue width per epilogue kind: 16 warps (64 accumulator
+// columns each) for the GELU + hi/lo-split FFN1 epilogue, whose per-tile work
+// bounds that GEMM; 8 elsewhere (the residual path needs the registers and the
+// 3-deep operand ring that the larger staging buffer would cost)
+__host__ __device__ constexpr int epi_groups2(int epi) { return epi == EPI_GELU_F16X ? 4 : 2; }
+
+template <int NA, int NB, int EPI>
 struct Cfg2 {
+    static constexpr int kEpiGroups2 = epi_groups2(EPI);
+    static constexpr int kThreads2 = 128 + 128 * kEpiGroups2;
+    static constexpr int kStageBufBytes2 = 4 * kEpiGroups2 * 32 * kStageLd * 4;
     static constexpr int kHalf = 128 * kBK * 2;  // 16 KB: one operand half-tile plane
     static constexpr int kStageBytes = (NA + NB) * kHalf;
-    static constexpr int kBudget = 227 * 1024 - 2048 - kStageBufBytes;
+    static constexpr int kBudget = 227 * 1024 - 2048 - kStageBufBytes2;
     static constexpr int kStagesRaw = kBudget / kStageBytes;
     static constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
-    static constexpr int kSmem = 1024 + kStages * kStageBytes + 256 + kStageBufBytes;
+    static constexpr int kSmem = 1024 + kStages * kStageBytes + 256 + kStageBufBytes2;
 };
 
 template <int NA, int NB, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<NA, NB, EPI>::kThreads2, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tA0, const __grid_constant__ CUtensorMap tA1,
                  const __grid_constant__ CUtensorMap tB0, const __grid_constant__ CUtensorMap tB1, GemmEpiParams p,
                  int64_t M, int64_t N, int64_t K) {
-    using C = Cfg2<NA, NB>;
+    using C = Cfg2<NA, NB, EPI>;
+    constexpr int kEpiGroups2 = C::kEpiGroups2;
     constexpr int BN = 256;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -618,7 +628,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 8 * kEpiGroups);  // epilogue warps of both CTAs (leader's copy is used)
+            mbar_init(&tempty[a], 8 * kEpiGroups2);  // epilogue warps of both CTAs (leader's copy is used)
         }
         fence_barrier_init();
     }
@@ -706,7 +716,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t taddr = tmem_base + ((quad * 32) << 16) + acc * BN;
             // this warp's column group; the next chunk's TMEM load overlaps the
             // current chunk's epilogue math (double-buffered registers)
-            const int cbeg = cg * (BN / kEpiGroups), cend = cbeg + BN / kEpiGroups;
+            const int cbeg = cg * (BN / kEpiGroups2), cend = cbeg + BN / kEpiGroups2;
             if (EPI == EPI_RESID) {
                 // residual reads do not depend on the MMA: the first chunk's are
                 // issued before waiting for the accumulator, each next chunk's
@@ -769,7 +779,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 template <int NA, int NB, int EPI>
 void launch2(const GemmArgs& g, int sm_count, cudaStream_t st) {
-    using C = Cfg2<NA, NB>;
+    using C = Cfg2<NA, NB, EPI>;
     auto kern = gemm2_kernel<NA, NB, EPI>;
     static bool attr_set = false;
     if (!attr_set) {
@@ -785,7 +795,7 @@ void launch2(const GemmArgs& g, int sm_count, cudaStream_t st) {
     if (NB == 1) b[1] = b[0];
     const int64_t tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256);
     int64_t clusters = tiles < sm_count / 2 ? tiles : sm_count / 2;
-    kern<<<(unsigned)(2 * clusters), kThreads, C::kSmem, st>>>(g.a[0], g.a[1], b[0], b[1], g.p, g.M, g.N, g.K);
+    kern<<<(unsigned)(2 * clusters), C::kThreads2, C::kSmem, st>>>(g.a[0], g.a[1], b[0], b[1], g.p, g.M, g.N, g.K);
     check_launch("gemm2_kernel");
 }
 
