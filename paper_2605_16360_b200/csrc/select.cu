@@ -26,7 +26,9 @@ __device__ __forceinline__ uint32_t order_key(float f) {
 }
 
 // Block-wide exclusive scan of one uint32 per thread; also returns the total.
+template <int kT = kThreads>
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* warp_sums, uint32_t& total) {
+    constexpr int kW = kT / 32;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t x = v;
 #pragma unroll
@@ -37,17 +39,17 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* warp_s
     if (lane == 31) warp_sums[warp] = x;
     __syncthreads();
     if (warp == 0) {
-        uint32_t w = warp_sums[lane];
+        uint32_t w = lane < (uint32_t)kW ? warp_sums[lane] : 0u;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
             if (lane >= (uint32_t)o) w += y;
         }
-        warp_sums[lane] = w;
+        if (lane < (uint32_t)kW) warp_sums[lane] = w;
     }
     __syncthreads();
     const uint32_t base = warp ? warp_sums[warp - 1] : 0u;
-    total = warp_sums[kWarps - 1];
+    total = warp_sums[kW - 1];
     __syncthreads();
     return base + x - v;
 }
@@ -207,22 +209,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 // and no key recomputation (the uncached kernel is ALU-bound on it).
 constexpr int kCacheTiles = 4;
 
-__global__ void __launch_bounds__(kThreads, 1)
+template <int kT>
+__global__ void __launch_bounds__(kT, 1024 / kT)
     topk_select_cached_kernel(const float* __restrict__ scores, int64_t n, int64_t k, uint8_t* __restrict__ mask,
                               int32_t* __restrict__ idx) {
-    __shared__ uint32_t hist[4096 + kWarps];  // + one discard bin per warp
-    __shared__ uint32_t warp_sums[kWarps];
+    __shared__ uint32_t hist[4096 + kT / 32];  // + one discard bin per warp
+    __shared__ uint32_t warp_sums[32];
     __shared__ uint32_t s_digit, s_above;
     const int tid = threadIdx.x;
     const int64_t slice = blockIdx.x;
     const int nn = (int)n;
     const uint32_t trash = 4096u + (uint32_t)(tid >> 5);
     const float* __restrict__ v = scores + slice * n;
-    const int ntiles = (nn + kThreads * kItems - 1) / (kThreads * kItems);
+    const int ntiles = (nn + kT * kItems - 1) / (kT * kItems);
     uint32_t key[kCacheTiles][kItems];
 #pragma unroll
     for (int t = 0; t < kCacheTiles; ++t) {
-        const int i0 = t * kThreads * kItems + tid * kItems;
+        const int i0 = t * kT * kItems + tid * kItems;
         if ((nn & 3) == 0 && i0 + kItems <= nn) {
             const float4 a = __ldcs(reinterpret_cast<const float4*>(v + i0));
             const float4 b = __ldcs(reinterpret_cast<const float4*>(v + i0 + 4));
@@ -241,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // per tile: number of this thread's items that exist
     auto nvalid = [&](int t) {
-        const int i0 = t * kThreads * kItems + tid * kItems;
+        const int i0 = t * kT * kItems + tid * kItems;
         const int r = nn - i0;
         return r <= 0 ? 0 : (r >= kItems ? kItems : r);
     };
@@ -251,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int bits = pass < 2 ? 12 : 8;
         const int shift = pass == 0 ? 20 : (pass == 1 ? 8 : 0);
         const uint32_t nb = 1u << bits, dmask = nb - 1;
-        for (uint32_t j = tid; j < nb; j += kThreads) hist[j] = 0;
+        for (uint32_t j = tid; j < nb; j += kT) hist[j] = 0;
         __syncthreads();
         // branch-free: non-candidates count into this warp's discard bin
         // (ATOMS.POPC.INC merges a warp's same-address increments)
@@ -266,29 +269,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         __syncthreads();
-        const uint32_t bpt = nb / kThreads;
-        uint32_t c[4] = {0, 0, 0, 0}, sum = 0;
-        if (bpt) {
+        // thread t owns bpt consecutive bins in descending digit order
+        constexpr int kBpt = 4096 / kT;  // bins per thread for the 12-bit digits
+        const int bpt = (int)(nb / kT) > 1 ? (int)(nb / kT) : 1;
+        uint32_t c[kBpt], sum = 0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                c[j] = hist[nb - 1 - (tid * 4 + j)];
-                sum += c[j];
-            }
-        } else if ((uint32_t)tid < nb) {
-            c[0] = hist[nb - 1 - tid];
-            sum = c[0];
+        for (int jj = 0; jj < kBpt; ++jj) {
+            const int bin = tid * bpt + jj;
+            c[jj] = (jj < bpt && bin < (int)nb) ? hist[nb - 1 - bin] : 0u;
+            sum += c[jj];
         }
         uint32_t total;
-        const uint32_t excl = block_excl_scan(sum, warp_sums, total);
+        const uint32_t excl = block_excl_scan<kT>(sum, warp_sums, total);
         if (excl < kr && kr <= excl + sum) {
             uint32_t acc = excl;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (acc < kr && kr <= acc + c[j]) {
-                    s_digit = nb - 1 - (uint32_t)(bpt ? tid * 4 + j : tid);
+            for (int jj = 0; jj < kBpt; ++jj) {
+                if (acc < kr && kr <= acc + c[jj]) {
+                    s_digit = nb - 1 - (uint32_t)(tid * bpt + jj);
                     s_above = acc;
                 }
-                acc += c[j];
+                acc += c[jj];
             }
         }
         __syncthreads();
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int t = 0; t < kCacheTiles; ++t) {
         if (t >= ntiles) break;
-        const int i0 = t * kThreads * kItems + tid * kItems;
+        const int i0 = t * kT * kItems + tid * kItems;
         const int nv = nvalid(t);
         uint32_t gt = 0, eq = 0;
 #pragma unroll
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ties go to the lowest indices: this thread takes the first
         // min(ties left - equal keys before it, #equal) of its own
         uint32_t tot;
-        const uint32_t excl = block_excl_scan((uint32_t)__popc(gt) | ((uint32_t)__popc(eq) << 16), warp_sums, tot);
+        const uint32_t excl = block_excl_scan<kT>((uint32_t)__popc(gt) | ((uint32_t)__popc(eq) << 16), warp_sums, tot);
         const uint32_t gt_excl = excl & 0xFFFFu, eq_excl = excl >> 16;
         const uint32_t ties_left = ties_taken - min(ties_taken, tie_base);
         const uint32_t tb = min(ties_left, eq_excl);                       // ties taken before this thread
@@ -351,8 +352,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 void launch_topk_select(const float* scores, int64_t slices, int64_t n, int64_t k, uint8_t* mask, int32_t* idx,
                         cudaStream_t st) {
     if (slices == 0) return;
-    if (n <= (int64_t)kThreads * kItems * kCacheTiles) {
-        topk_select_cached_kernel<<<(unsigned)slices, kThreads, 0, st>>>(scores, n, k, mask, idx);
+    // register-cached rows: the smallest CTA that holds the row (more CTAs per
+    // SM and shorter block scans for short rows)
+    if (n <= 256 * kItems * kCacheTiles) {
+        topk_select_cached_kernel<256><<<(unsigned)slices, 256, 0, st>>>(scores, n, k, mask, idx);
+    } else if (n <= 512 * kItems * kCacheTiles) {
+        topk_select_cached_kernel<512><<<(unsigned)slices, 512, 0, st>>>(scores, n, k, mask, idx);
+    } else if (n <= (int64_t)kThreads * kItems * kCacheTiles) {
+        topk_select_cached_kernel<kThreads><<<(unsigned)slices, kThreads, 0, st>>>(scores, n, k, mask, idx);
     } else {
         topk_select_kernel<<<(unsigned)slices, kThreads, 0, st>>>(scores, n, k, mask, idx);
     }
