@@ -8,7 +8,10 @@ uses. The fp64 oracle cannot score 32k x 32k x 32 heads x 16 layers on CPU, so:
     for the 4 target layers paired with them: norm-wise rel <= 1e-3 and Top-K
     (rho = 0.2, K = 6554) index overlap >= 99.9% (mean), min reported;
   * select + compaction at full size: bit-exact vs the oracle restatement
-    driven from the GPU's Ŷ (all 256 slices)."""
+    driven from the GPU's Ŷ (all 256 slices);
+  * configs[2] / [3] scoring at their full contexts (131072 keys with GQA 7;
+    65536 keys at head_dim 128) on 2 proxy layers: sampled-query LSE vs the
+    fp64 restatement and sampled-key X vs float64 over all queries."""
 import numpy as np
 import pytest
 
@@ -91,3 +94,39 @@ def test_fullsize_select_compaction_bit_exact(run):
     eko, evo = O.compact_kv(kt, vt, oidx[sl])
     np.testing.assert_array_equal(_bits(run["ko"]).reshape(S, K, c["dt"])[sl], eko)
     np.testing.assert_array_equal(_bits(run["vo"]).reshape(S, K, c["dt"])[sl], evo)
+
+
+@pytest.mark.parametrize("name", ["qwen25_128k", "qwen3_64k"])
+def test_fullsize_scoring_other_configs(gpu, name):
+    """BASELINE configs[2] / [3] scoring at full context (GQA 7 at d 64 over
+    131072 keys; d 128 over 65536 keys), 2 of the proxy layers: the pass-1 LSE
+    of sampled queries vs the fp64 restatement, and the pooled X of sampled
+    keys vs a float64 evaluation over ALL queries of the group (using the
+    GPU's LSE, itself checked above): rel 1e-3 of the slab's max."""
+    import torch
+    import bench
+    import paper_2605_16360_b200 as P
+    c = dict(bench.CONFIGS[name])
+    c["Ls"] = 2
+    q, kp, _, _ = bench.make_inputs(dict(c, Ll=1, Hl=1, dt=8), torch.device("cuda"), 77)
+    x = P.score(q, kp, ctx=gpu)
+    lse = P.score_lse(q, kp, ctx=gpu)
+    torch.cuda.synchronize()
+    g, d, N = c["Hq"] // c["Hs"], c["dp"], c["N"]
+    rs = np.random.RandomState(1)
+    for l, kh in [(0, 0), (1, c["Hs"] - 1)]:
+        qb = _bits(q[l, kh * g:(kh + 1) * g])
+        kb = _bits(kp[l, kh:kh + 1])
+        qi = np.sort(rs.choice(N, 48, replace=False))
+        want = O.score_lse(qb[None, :1, qi], kb[None])[0, 0]
+        got = lse[l, kh * g, qi].cpu().numpy()
+        assert np.abs(got - want).max() < 2e-4, (name, np.abs(got - want).max())
+        # X at sampled keys, float64 over every query of the group
+        qf = q[l, kh * g:(kh + 1) * g].double()             # [g, N, d]
+        ks = np.sort(rs.choice(N, 24, replace=False))
+        kf = kp[l, kh, torch.from_numpy(ks).cuda()].double()  # [24, d]
+        s = torch.einsum("gnd,kd->gnk", qf, kf) / d ** 0.5 - lse[l, kh * g:(kh + 1) * g].double()[..., None]
+        xw = torch.exp(s.amax(dim=(0, 1))).cpu().numpy()
+        xg = x[l, kh, torch.from_numpy(ks).cuda()].double().cpu().numpy()
+        scale = x[l, kh].max().item()
+        assert np.abs(xg - xw).max() <= 1e-3 * scale, (name, np.abs(xg - xw).max() / scale)
