@@ -89,6 +89,25 @@ pkv_status pkv_topk_overlap(pkv_ctx ctx, const uint8_t* mask_a_dev, const uint8_
 pkv_status pkv_captured_mass(pkv_ctx ctx, const uint8_t* mask_pred_dev, const float* y_dev, int64_t slices,
                              int64_t n, int64_t k, double* per_slice_out_dev, void* stream);
 
+/* Spearman rank correlation per slice (replaces spearman_per_slice,
+ * pruning.cpp:173-186): Pearson correlation of the average ranks (ties share
+ * the mean of their 1-based positions, pruning.cpp:122-140) of a and b,
+ * fp32 rows [slices, n] (−0 ties with +0, as the reference's double compare);
+ * 1 when both rows are constant, 0 when exactly one is. n >= 2 (PKV_EVALUE
+ * otherwise, the reference's ValueError). The sums are exact integers; the one
+ * rounding is the final division. */
+pkv_status pkv_spearman(pkv_ctx ctx, const float* a_dev, const float* b_dev, int64_t slices, int64_t n,
+                        double* per_slice_out_dev, void* stream);
+
+/* One MetricAccumulator::add sample on the device (pruning.cpp:218-247):
+ * both Top-K masks at k = retention_count(rho, n), then per slice the
+ * captured mass of y_pred's mask in y_true, the Top-K overlap of the two
+ * masks and the Spearman correlation of y_pred vs y_true. The running means
+ * over samples (MetricAccumulator::report) are host arithmetic. */
+pkv_status pkv_slice_metrics(pkv_ctx ctx, const float* y_pred_dev, const float* y_true_dev, int64_t slices, int64_t n,
+                             int64_t k, double* mass_out_dev, double* overlap_out_dev, double* spearman_out_dev,
+                             void* stream);
+
 /* --------------------------------------------------- compaction (a-4) ---- */
 /* Packed KV gather in apply_mask order (no reference code; the reference only
  * reports indices, pruning.cpp:197-215): for s < slices, j < k,

@@ -451,6 +451,47 @@ def topk_overlap_per_slice(mask_a: np.ndarray, mask_b: np.ndarray, k: int) -> np
     return (a & b).sum(axis=1) / float(k)
 
 
+def average_ranks(v: np.ndarray) -> np.ndarray:
+    """pruning.cpp:122-140: 1-based ranks along the last axis, ties sharing the
+    mean of their positions (a stable sort; -0.0 == +0.0 as in a double compare)."""
+    v = np.asarray(v, np.float64) + 0.0  # folds -0.0 onto +0.0
+    n = v.shape[-1]
+    flat = v.reshape(-1, n)
+    out = np.empty_like(flat)
+    for s in range(flat.shape[0]):
+        order = np.argsort(flat[s], kind="stable")
+        sv = flat[s][order]
+        head = np.r_[True, sv[1:] != sv[:-1]]
+        start = np.maximum.accumulate(np.where(head, np.arange(n), 0))
+        tail = np.r_[sv[1:] != sv[:-1], True]
+        end = np.minimum.accumulate(np.where(tail, np.arange(n), n)[::-1])[::-1]
+        out[s, order] = 0.5 * (start + end) + 1.0
+    return out.reshape(v.shape)
+
+
+def spearman_per_slice(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """pruning.cpp:142-186: Pearson of the average ranks per slice; 1 when both
+    slices are constant, 0 when exactly one is."""
+    n = a.shape[-1]
+    if a.shape != b.shape:
+        raise ValueError("spearman shapes differ")
+    if n < 2:
+        raise ValueError("spearman needs at least two tokens per slice")
+    ra = average_ranks(a).reshape(-1, n)
+    rb = average_ranks(b).reshape(-1, n)
+    out = np.empty(ra.shape[0])
+    for s in range(ra.shape[0]):
+        da, db = ra[s] - ra[s].mean(), rb[s] - rb[s].mean()
+        saa, sbb = (da * da).sum(), (db * db).sum()
+        if saa == 0.0 and sbb == 0.0:
+            out[s] = 1.0
+        elif saa == 0.0 or sbb == 0.0:
+            out[s] = 0.0
+        else:
+            out[s] = (da * db).sum() / np.sqrt(saa * sbb)
+    return out
+
+
 # ---------------------------------------------------- compiled reference ----
 class RefLib:
     """ctypes view of oracle/_ref/libpkvref.so: the UNMODIFIED reference compiled here."""
@@ -525,6 +566,17 @@ class RefLib:
         self.L.pkvref_captured_mass_per_slice.argtypes = [_u8p, ctypes.c_int64, _f64p, _i64p, ctypes.c_int, _f64p]
         self._check(self.L.pkvref_captured_mass_per_slice(_ptr(pb, _u8p), k, _ptr(yy, _f64p), _ptr(shape, _i64p),
                                                           yy.ndim, _ptr(out, _f64p)))
+        return out
+
+    def spearman_per_slice(self, a: np.ndarray, b: np.ndarray) -> np.ndarray:
+        """The reference's spearman_per_slice (pruning.cpp:173-186)."""
+        aa = np.ascontiguousarray(a, np.float64)
+        bb = np.ascontiguousarray(b, np.float64)
+        shape = np.array(aa.shape, np.int64)
+        out = np.zeros(aa.size // aa.shape[-1], np.float64)
+        self.L.pkvref_spearman_per_slice.argtypes = [_f64p, _f64p, _i64p, ctypes.c_int, _f64p]
+        self._check(self.L.pkvref_spearman_per_slice(_ptr(aa, _f64p), _ptr(bb, _f64p), _ptr(shape, _i64p), aa.ndim,
+                                                     _ptr(out, _f64p)))
         return out
 
     def apply_mask(self, bits: np.ndarray, k: int, head_dim: int, bytes_per_elem: int = 2):

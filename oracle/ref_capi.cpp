@@ -136,6 +136,14 @@ int pkvref_captured_mass_per_slice(const uint8_t* pred, int64_t k, const double*
     });
 }
 
+// spearman_per_slice (pruning.cpp:173-186) of two fp64 tensors of one shape
+int pkvref_spearman_per_slice(const double* a, const double* b, const int64_t* shape, int rank, double* out) {
+    return guard([&] {
+        const auto v = spearman_per_slice(make_tensor(a, shape, rank), make_tensor(b, shape, rank));
+        std::memcpy(out, v.data(), v.size() * sizeof(double));
+    });
+}
+
 int pkvref_layer_pair(int64_t target_layer, const int64_t* geom5, int64_t* out) {
     return guard([&] {
         ModelGeometry g{geom5[0], geom5[1], geom5[2], geom5[3], geom5[4]};

@@ -82,6 +82,8 @@ SIGNATURES = {
     "pkv_topk_mask_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_dbl, _c_vp, _c_i64p]),
     "pkv_topk_overlap": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp]),
     "pkv_captured_mass": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp]),
+    "pkv_spearman": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_vp, _c_vp]),
+    "pkv_slice_metrics": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
     "pkv_compact_kv": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_vp,
                                       _c_vp, _c_vp]),
     "pkv_score": (ctypes.c_int, [_c_vp, _c_vp, _c_vp] + [_c_i64] * 6 + [_c_u32, _c_vp, _c_vp, _c_vp]),

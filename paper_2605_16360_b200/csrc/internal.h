@@ -78,6 +78,7 @@ struct pkv_ctx_s {
     pkv::DevBuf scratch_host_io;
     pkv::DevBuf scratch_score;
     pkv::DevBuf scratch_decode;
+    pkv::DevBuf scratch_metrics;
 };
 
 namespace pkv {

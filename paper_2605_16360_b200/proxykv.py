@@ -24,6 +24,7 @@ __all__ = [
     "Context", "PruneMask", "MaskApplication", "ModelGeometry", "MapperConfig", "Mapper", "Pruner",
     "retention_count", "topk_select", "topk_mask", "apply_mask", "compact_kv", "score", "score_lse",
     "proxy_prefill_attention", "packed_decode_attention", "topk_overlap_device", "captured_mass_device",
+    "spearman_device", "slice_metrics_device", "MetricAccumulator", "MetricReport",
     "layer_pair", "window_offsets", "mapper_init_params", "ShapeError", "PkvValueError", "ConfigError",
     "CudaError", "NoDeviceError", "PkvError", "SCORE_REDUCE_MAX", "SCORE_REDUCE_SUM", "SCORE_CAUSAL",
     "MAPPER_FP16", "MAPPER_FP16X2", "MAPPER_FP16X3", "SHARD_LAYER", "SHARD_HEAD", "ShardPlan", "shard_plan",
@@ -184,6 +185,89 @@ def captured_mass_device(mask_pred, y, k: int, *, ctx: Context = None, stream=No
     check(lib().pkv_captured_mass(ctx.h, _ptr(mask_pred.contiguous()), _ptr(y.contiguous()), slices, n, int(k),
                                   _ptr(out), _stream(stream)))
     return out
+
+
+def spearman_device(a, b, *, ctx: Context = None, stream=None):
+    """pruning.cpp:173-186 on the device: per-slice Spearman correlation of two
+    fp32 cuda tensors [..., n] with average ranks on ties (fp64 cuda tensor)."""
+    torch = _torch()
+    ctx = ctx or Context.default(a.device.index or 0)
+    if a.shape != b.shape:
+        raise ShapeError(f"spearman shapes differ: {tuple(a.shape)} vs {tuple(b.shape)}")
+    n = a.shape[-1]
+    slices = a.numel() // n
+    out = torch.empty(slices, dtype=torch.float64, device=a.device)
+    check(lib().pkv_spearman(ctx.h, _ptr(a.contiguous()), _ptr(b.contiguous()), slices, n, _ptr(out),
+                             _stream(stream)))
+    return out
+
+
+def slice_metrics_device(y_pred, y_true, rho: float, *, ctx: Context = None, stream=None):
+    """One MetricAccumulator::add sample (pruning.cpp:218-247) on the device:
+    (captured mass, Top-K overlap, Spearman) per slice, fp64 cuda tensors."""
+    torch = _torch()
+    ctx = ctx or Context.default(y_pred.device.index or 0)
+    if y_pred.shape != y_true.shape:
+        raise ShapeError(f"metric shapes differ: {tuple(y_pred.shape)} vs {tuple(y_true.shape)}")
+    n = y_pred.shape[-1]
+    slices = y_pred.numel() // n
+    k = retention_count(rho, n)
+    outs = [torch.empty(slices, dtype=torch.float64, device=y_pred.device) for _ in range(3)]
+    check(lib().pkv_slice_metrics(ctx.h, _ptr(y_pred.contiguous()), _ptr(y_true.contiguous()), slices, n, k,
+                                  _ptr(outs[0]), _ptr(outs[1]), _ptr(outs[2]), _stream(stream)))
+    return tuple(outs)
+
+
+@dataclass
+class MetricReport:
+    """pruning.hpp MetricReport: means over samples per (layer, head) and overall."""
+    rho: float
+    captured_mass: float
+    topk_overlap: float
+    spearman: float
+    per_slice_mass: list
+    per_slice_overlap: list
+    per_slice_spearman: list
+
+
+class MetricAccumulator:
+    """MetricAccumulator (pruning.cpp:218-275) with the per-sample work on the
+    device (pkv_slice_metrics); only the running sums are host arithmetic.
+    add() takes [B, L, H, N] or [L, H, N] fp32 cuda tensors."""
+
+    def __init__(self, rho: float, *, ctx: Context = None):
+        self.rho = float(rho)
+        self.ctx = ctx
+        self._sums = None
+        self._counts = None
+        self._slices = 0
+
+    def add(self, y_pred, y_true, stream=None):
+        torch = _torch()
+        if y_pred.shape != y_true.shape:
+            raise ShapeError(f"metric shapes differ: {tuple(y_pred.shape)} vs {tuple(y_true.shape)}")
+        if y_pred.dim() not in (3, 4):
+            raise ShapeError(f"metrics expect [B, L, H, N] or [L, H, N], got {tuple(y_pred.shape)}")
+        b = y_pred.shape[0] if y_pred.dim() == 4 else 1
+        lh = y_pred.numel() // y_pred.shape[-1] // b
+        if self._slices == 0:
+            self._slices = lh
+            self._sums = torch.zeros(3, lh, dtype=torch.float64, device=y_pred.device)
+            self._counts = 0
+        if lh != self._slices:
+            raise ShapeError("inconsistent (layer, head) slice count across samples")
+        m, o, s = slice_metrics_device(y_pred, y_true, self.rho, ctx=self.ctx, stream=stream)
+        # samples are added in batch order, slice key = i % lh (pruning.cpp:240-245)
+        self._sums += torch.stack([m, o, s]).view(3, b, lh).sum(dim=1)
+        self._counts += b
+
+    def report(self) -> MetricReport:
+        if self._slices == 0:
+            raise PkvValueError("no samples accumulated")
+        per = (self._sums / float(self._counts)).cpu().numpy()
+        lh = float(self._slices)
+        return MetricReport(self.rho, float(sum(per[0].tolist()) / lh), float(sum(per[1].tolist()) / lh),
+                            float(sum(per[2].tolist()) / lh), per[0].tolist(), per[1].tolist(), per[2].tolist())
 
 
 def compact_kv(k_in, v_in, idx_asc, *, ctx: Context = None, stream=None, out=None):

@@ -105,6 +105,36 @@ def test_topk_differential_vs_reference():
         np.testing.assert_array_equal(idx, ridx)
 
 
+# ---------------------------------------------------------------- spearman --
+def test_spearman_reference_known_answers():
+    """test_pruning.cpp:155-167: identity 1, reversal -1, average ranks on ties
+    (a = [1, 2, 2, 3] -> [1, 2.5, 2.5, 4]) vs [1, 2, 3, 4] = 0.9486832980505138."""
+    y = np.array([[[0.1, 0.9, 0.3, 0.7, 0.5]]])
+    rev = np.array([[[0.9, 0.1, 0.7, 0.3, 0.5]]])
+    assert O.spearman_per_slice(y, y)[0] == pytest.approx(1.0)
+    assert O.spearman_per_slice(y, rev)[0] == pytest.approx(-1.0)
+    np.testing.assert_array_equal(O.average_ranks(np.array([1.0, 2, 2, 3])), [1, 2.5, 2.5, 4])
+    assert O.spearman_per_slice(np.array([[1.0, 2, 2, 3]]), np.array([[1.0, 2, 3, 4]]))[0] == \
+        pytest.approx(0.9486832980505138)
+    assert O.spearman_per_slice(np.ones((1, 4)), np.ones((1, 4)))[0] == 1.0
+    assert O.spearman_per_slice(np.ones((1, 4)), np.arange(4.0)[None])[0] == 0.0
+    with pytest.raises(ValueError):
+        O.spearman_per_slice(np.ones((1, 1)), np.ones((1, 1)))
+
+
+def test_spearman_differential_vs_reference():
+    ref = O.RefLib()
+    r = np.random.RandomState(5)
+    for shape in [(1, 2), (3, 7), (2, 3, 1000), (2, 4099)]:
+        a = np.floor(r.rand(*shape) * 16) - 8.0  # heavy ties, signed zeros below
+        b = a + r.standard_normal(shape) * 3
+        a[..., ::7] = -0.0
+        np.testing.assert_allclose(O.spearman_per_slice(a, b), ref.spearman_per_slice(a, b), rtol=0, atol=1e-13)
+    c = np.zeros((2, 5))
+    c[1] = np.arange(5)
+    np.testing.assert_array_equal(ref.spearman_per_slice(c, np.zeros((2, 5))), [1.0, 0.0])
+
+
 # ----------------------------------------------------------- compaction ----
 def test_compact_kv_gathers_in_index_order():
     r = np.random.RandomState(0)
