@@ -108,6 +108,36 @@ pkv_status pkv_slice_metrics(pkv_ctx ctx, const float* y_pred_dev, const float* 
                              int64_t k, double* mass_out_dev, double* overlap_out_dev, double* spearman_out_dev,
                              void* stream);
 
+/* Training loss suite on the device (replaces
+ * loss_total, loss.cpp:324-374, with loss_bin / loss_mse / loss_fine /
+ * loss_global / loss_cos and their pair sampling, loss.cpp:53-322): logits and
+ * ground-truth scores fp32 [shape] on the device (the reference's fp64 inputs
+ * must be fp32-representable for parity), computed in fp64. The pair samples
+ * are the reference's own (same xoshiro256** streams per slice, same partial
+ * Fisher-Yates / Floyd sampling, same filter), so used / filtered counts match
+ * exactly. grad_dev (nullable, fp64 [shape]) receives d total / d logits — what
+ * the reference's tape computes for report.total_tensor.backward().
+ * Errors: LossConfig::validate's messages (PKV_EVALUE), "degenerate oracle"
+ * when max(y) <= 0. Synchronises the stream (the report is host memory). */
+typedef struct {
+    double lambda_mse, lambda_bin, lambda_fine, lambda_global, lambda_cos;
+    const double* ratios; /* host array */
+    int64_t n_ratios;
+    double gamma, epsilon, mse_exponent, margin, clip_lo, clip_hi, pair_filter_frac, topk_ratio_for_rank;
+    int64_t max_pairs;
+} pkv_loss_config;
+
+typedef struct {
+    double bin, mse, fine, global, cos;
+    double weighted_bin, weighted_mse, weighted_fine, weighted_global, weighted_cos;
+    double total, s_max;
+    int64_t fine_used, fine_filtered, global_used, global_filtered, cos_floor_hits;
+} pkv_loss_report;
+
+pkv_status pkv_loss_total(pkv_ctx ctx, const float* logits_dev, const float* y_dev, const int64_t* shape, int rank,
+                          const pkv_loss_config* cfg, uint64_t seed, pkv_loss_report* report_out, double* grad_dev,
+                          void* stream);
+
 /* --------------------------------------------------- compaction (a-4) ---- */
 /* Packed KV gather in apply_mask order (no reference code; the reference only
  * reports indices, pruning.cpp:197-215): for s < slices, j < k,

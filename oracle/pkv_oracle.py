@@ -579,6 +579,32 @@ class RefLib:
                                                      _ptr(out, _f64p)))
         return out
 
+    def loss_total(self, logits: np.ndarray, y: np.ndarray, cfg, seed: int, want_grad: bool = True):
+        """The reference's loss_total (loss.cpp:324-374) and, through its tape,
+        d total / d logits. cfg: any object with LossConfig's field names."""
+        z = np.ascontiguousarray(logits, np.float64)
+        yy = np.ascontiguousarray(y, np.float64)
+        shape = np.array(z.shape, np.int64)
+        cf = np.array([cfg.lambda_mse, cfg.lambda_bin, cfg.lambda_fine, cfg.lambda_global, cfg.lambda_cos, cfg.gamma,
+                       cfg.epsilon, cfg.mse_exponent, cfg.margin, cfg.clip_lo, cfg.clip_hi, cfg.pair_filter_frac,
+                       cfg.topk_ratio_for_rank], np.float64)
+        ratios = np.ascontiguousarray(cfg.ratios, np.float64)
+        rep = np.zeros(12, np.float64)
+        cnt = np.zeros(5, np.int64)
+        grad = np.zeros_like(z) if want_grad else None
+        self.L.pkvref_loss_total.argtypes = [_f64p, _f64p, _i64p, ctypes.c_int, _f64p, _f64p, ctypes.c_int64,
+                                             ctypes.c_int64, ctypes.c_uint64, _f64p, _i64p, ctypes.c_void_p]
+        self._check(self.L.pkvref_loss_total(_ptr(z, _f64p), _ptr(yy, _f64p), _ptr(shape, _i64p), z.ndim,
+                                             _ptr(cf, _f64p), _ptr(ratios, _f64p), len(ratios), int(cfg.max_pairs),
+                                             seed, _ptr(rep, _f64p), _ptr(cnt, _i64p),
+                                             grad.ctypes.data if want_grad else None))
+        names = ["bin", "mse", "fine", "global", "cos", "weighted_bin", "weighted_mse", "weighted_fine",
+                 "weighted_global", "weighted_cos", "total", "s_max"]
+        out = dict(zip(names, rep.tolist()))
+        out.update(fine_used=int(cnt[0]), fine_filtered=int(cnt[1]), global_used=int(cnt[2]),
+                   global_filtered=int(cnt[3]), cos_floor_hits=int(cnt[4]))
+        return out, grad
+
     def apply_mask(self, bits: np.ndarray, k: int, head_dim: int, bytes_per_elem: int = 2):
         b = np.ascontiguousarray(bits, np.uint8)
         shape = np.array(b.shape, np.int64)

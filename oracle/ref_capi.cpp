@@ -16,6 +16,7 @@
 #include "proxykv/common.hpp"
 #include "proxykv/mapper.hpp"
 #include "proxykv/pruning.hpp"
+#include "proxykv/loss.hpp"
 #include "proxykv/rng.hpp"
 #include "proxykv/tensor.hpp"
 
@@ -141,6 +142,55 @@ int pkvref_spearman_per_slice(const double* a, const double* b, const int64_t* s
     return guard([&] {
         const auto v = spearman_per_slice(make_tensor(a, shape, rank), make_tensor(b, shape, rank));
         std::memcpy(out, v.data(), v.size() * sizeof(double));
+    });
+}
+
+// loss_total (loss.cpp:324-374) + the tape's gradient w.r.t. the logits.
+// cfgd = {lambda_mse, lambda_bin, lambda_fine, lambda_global, lambda_cos, gamma,
+//         epsilon, mse_exponent, margin, clip_lo, clip_hi, pair_filter_frac,
+//         topk_ratio_for_rank}; rep = {bin, mse, fine, global, cos, w_bin, w_mse,
+//         w_fine, w_global, w_cos, total, s_max}; cnt = {fine used, fine
+//         filtered, global used, global filtered, cos floor hits}.
+int pkvref_loss_total(const double* logits, const double* y, const int64_t* shape, int rank, const double* cfgd,
+                      const double* ratios, int64_t n_ratios, int64_t max_pairs, uint64_t seed, double* rep,
+                      int64_t* cnt, double* grad) {
+    return guard([&] {
+        LossConfig c;
+        c.lambda_mse = cfgd[0];
+        c.lambda_bin = cfgd[1];
+        c.lambda_fine = cfgd[2];
+        c.lambda_global = cfgd[3];
+        c.lambda_cos = cfgd[4];
+        c.gamma = cfgd[5];
+        c.epsilon = cfgd[6];
+        c.mse_exponent = cfgd[7];
+        c.margin = cfgd[8];
+        c.clip_lo = cfgd[9];
+        c.clip_hi = cfgd[10];
+        c.pair_filter_frac = cfgd[11];
+        c.topk_ratio_for_rank = cfgd[12];
+        c.ratios.assign(ratios, ratios + n_ratios);
+        c.max_pairs = max_pairs;
+        Tensor z = make_tensor(logits, shape, rank);
+        z.set_requires_grad(true);
+        const LossReport r = loss_total(z, make_tensor(y, shape, rank), c, seed);
+        const double v[12] = {r.bin, r.mse, r.fine, r.global, r.cos, r.weighted_bin, r.weighted_mse,
+                              r.weighted_fine, r.weighted_global, r.weighted_cos, r.total, r.s_max};
+        std::memcpy(rep, v, sizeof(v));
+        cnt[0] = r.fine_pairs.used;
+        cnt[1] = r.fine_pairs.filtered;
+        cnt[2] = r.global_pairs.used;
+        cnt[3] = r.global_pairs.filtered;
+        cnt[4] = r.cos_floor_hits;
+        if (grad) {
+            const size_t n = static_cast<size_t>(z.numel());
+            if (r.total_tensor.defined()) {
+                r.total_tensor.backward();
+                std::memcpy(grad, z.grad().data(), n * sizeof(double));
+            } else {
+                std::memset(grad, 0, n * sizeof(double));
+            }
+        }
     });
 }
 

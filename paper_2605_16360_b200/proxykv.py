@@ -25,6 +25,7 @@ __all__ = [
     "retention_count", "topk_select", "topk_mask", "apply_mask", "compact_kv", "score", "score_lse",
     "proxy_prefill_attention", "packed_decode_attention", "topk_overlap_device", "captured_mass_device",
     "spearman_device", "slice_metrics_device", "MetricAccumulator", "MetricReport",
+    "LossConfig", "LossReport", "loss_total",
     "layer_pair", "window_offsets", "mapper_init_params", "ShapeError", "PkvValueError", "ConfigError",
     "CudaError", "NoDeviceError", "PkvError", "SCORE_REDUCE_MAX", "SCORE_REDUCE_SUM", "SCORE_CAUSAL",
     "MAPPER_FP16", "MAPPER_FP16X2", "MAPPER_FP16X3", "SHARD_LAYER", "SHARD_HEAD", "ShardPlan", "shard_plan",
@@ -268,6 +269,92 @@ class MetricAccumulator:
         lh = float(self._slices)
         return MetricReport(self.rho, float(sum(per[0].tolist()) / lh), float(sum(per[1].tolist()) / lh),
                             float(sum(per[2].tolist()) / lh), per[0].tolist(), per[1].tolist(), per[2].tolist())
+
+
+@dataclass
+class LossConfig:
+    """loss.hpp LossConfig (same fields, same defaults)."""
+    lambda_mse: float = 20.0
+    lambda_bin: float = 10.0
+    lambda_fine: float = 3.0
+    lambda_global: float = 2.0
+    lambda_cos: float = 0.5
+    ratios: Sequence[float] = (0.05, 0.1, 0.15, 0.2, 0.3, 0.4, 0.5)
+    gamma: float = 1.0
+    epsilon: float = 0.1
+    mse_exponent: float = 1.5
+    margin: float = 1.0
+    clip_lo: float = 1.0
+    clip_hi: float = 5.0
+    pair_filter_frac: float = 0.01
+    topk_ratio_for_rank: float = 0.2
+    max_pairs: int = 4096
+
+
+class _CLossConfig(ctypes.Structure):
+    _fields_ = [("lambda_mse", ctypes.c_double), ("lambda_bin", ctypes.c_double), ("lambda_fine", ctypes.c_double),
+                ("lambda_global", ctypes.c_double), ("lambda_cos", ctypes.c_double),
+                ("ratios", ctypes.POINTER(ctypes.c_double)), ("n_ratios", ctypes.c_int64),
+                ("gamma", ctypes.c_double), ("epsilon", ctypes.c_double), ("mse_exponent", ctypes.c_double),
+                ("margin", ctypes.c_double), ("clip_lo", ctypes.c_double), ("clip_hi", ctypes.c_double),
+                ("pair_filter_frac", ctypes.c_double), ("topk_ratio_for_rank", ctypes.c_double),
+                ("max_pairs", ctypes.c_int64)]
+
+
+class _CLossReport(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("bin", "mse", "fine", "global_", "cos", "weighted_bin", "weighted_mse",
+                                               "weighted_fine", "weighted_global", "weighted_cos", "total",
+                                               "s_max")] + \
+               [(n, ctypes.c_int64) for n in ("fine_used", "fine_filtered", "global_used", "global_filtered",
+                                              "cos_floor_hits")]
+
+
+@dataclass
+class LossReport:
+    """loss.hpp LossReport (total_tensor -> the gradient returned beside it)."""
+    bin: float
+    mse: float
+    fine: float
+    global_: float
+    cos: float
+    weighted_bin: float
+    weighted_mse: float
+    weighted_fine: float
+    weighted_global: float
+    weighted_cos: float
+    total: float
+    s_max: float
+    fine_used: int
+    fine_filtered: int
+    global_used: int
+    global_filtered: int
+    cos_floor_hits: int
+
+
+def loss_total(logits, y, cfg: LossConfig = None, seed: int = 0, *, want_grad: bool = True, ctx: Context = None,
+               stream=None):
+    """loss_total (loss.cpp:324-374) on the device: fp32 cuda logits / scores
+    of one shape -> (LossReport, d total / d logits as an fp64 cuda tensor or
+    None). The pair samples are the reference's own for the same seed."""
+    torch = _torch()
+    cfg = cfg or LossConfig()
+    ctx = ctx or Context.default(logits.device.index or 0)
+    if logits.shape != y.shape:
+        raise ShapeError(f"loss_total shapes differ: {tuple(logits.shape)} vs {tuple(y.shape)}")
+    if logits.dtype != torch.float32 or y.dtype != torch.float32 or not logits.is_cuda:
+        raise ShapeError("loss_total expects float32 CUDA tensors")
+    ratios = (ctypes.c_double * max(1, len(cfg.ratios)))(*cfg.ratios)
+    c = _CLossConfig(cfg.lambda_mse, cfg.lambda_bin, cfg.lambda_fine, cfg.lambda_global, cfg.lambda_cos,
+                     ctypes.cast(ratios, ctypes.POINTER(ctypes.c_double)) if len(cfg.ratios) else None,
+                     len(cfg.ratios), cfg.gamma, cfg.epsilon, cfg.mse_exponent, cfg.margin, cfg.clip_lo, cfg.clip_hi,
+                     cfg.pair_filter_frac, cfg.topk_ratio_for_rank, int(cfg.max_pairs))
+    shape = (ctypes.c_int64 * logits.dim())(*logits.shape)
+    rep = _CLossReport()
+    grad = torch.empty(logits.shape, dtype=torch.float64, device=logits.device) if want_grad else None
+    check(lib().pkv_loss_total(ctx.h, _ptr(logits.contiguous()), _ptr(y.contiguous()), shape, logits.dim(),
+                               ctypes.byref(c), ctypes.c_uint64(seed), ctypes.byref(rep),
+                               _ptr(grad) if want_grad else None, _stream(stream)))
+    return LossReport(*[getattr(rep, f[0]) for f in _CLossReport._fields_]), grad
 
 
 def compact_kv(k_in, v_in, idx_asc, *, ctx: Context = None, stream=None, out=None):
