@@ -18,3 +18,8 @@ P.slice_metrics_device(a, b, 0.2, ctx=ctx, stream=st)  # grow the scratch once
 t1 = bench.time_loop(lambda: P.spearman_device(a, b, ctx=ctx, stream=st), 5, st)
 t2 = bench.time_loop(lambda: P.slice_metrics_device(a, b, 0.2, ctx=ctx, stream=st), 5, st)
 print(f"spearman {S}x{n}: {t1:.3f} ms; slice_metrics (mass+overlap+spearman): {t2:.3f} ms")
+z = torch.randn(1, 32, 8, n, device="cuda")
+y = torch.rand(1, 32, 8, n, device="cuda")
+P.loss_total(z, y, P.LossConfig(), 7, ctx=ctx)
+t3 = bench.time_loop(lambda: P.loss_total(z, y, P.LossConfig(), 7, ctx=ctx), 3, st)
+print(f"loss_total + grad [1, 32, 8, {n}]: {t3:.3f} ms")
