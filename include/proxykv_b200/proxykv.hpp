@@ -213,4 +213,38 @@ private:
     ModelGeometry geom_;
 };
 
+// pruning.cpp:173-186 over DEVICE fp32 rows [slices, n] -> DEVICE fp64 [slices]
+inline void spearman_per_slice(const Context& ctx, const float* a_dev, const float* b_dev, int64_t slices, int64_t n,
+                               double* out_dev, void* stream = nullptr) {
+    check(pkv_spearman(ctx.get(), a_dev, b_dev, slices, n, out_dev, stream));
+}
+
+// loss.hpp:16-37 (same fields, same defaults)
+struct LossConfig {
+    double lambda_mse = 20.0, lambda_bin = 10.0, lambda_fine = 3.0, lambda_global = 2.0, lambda_cos = 0.5;
+    std::vector<double> ratios = {0.05, 0.1, 0.15, 0.2, 0.3, 0.4, 0.5};
+    double gamma = 1.0, epsilon = 0.1, mse_exponent = 1.5, margin = 1.0, clip_lo = 1.0, clip_hi = 5.0;
+    double pair_filter_frac = 0.01, topk_ratio_for_rank = 0.2;
+    int64_t max_pairs = 4096;
+    // the C view borrows `ratios`: valid while this LossConfig lives
+    pkv_loss_config c() const {
+        return pkv_loss_config{lambda_mse, lambda_bin, lambda_fine, lambda_global, lambda_cos, ratios.data(),
+                               static_cast<int64_t>(ratios.size()), gamma, epsilon, mse_exponent, margin, clip_lo,
+                               clip_hi, pair_filter_frac, topk_ratio_for_rank, max_pairs};
+    }
+};
+using LossReport = pkv_loss_report;
+
+// loss.cpp:324-374 over DEVICE fp32 logits / scores; grad_dev (fp64, nullable)
+// receives d total / d logits (the reference's total_tensor.backward()).
+inline LossReport loss_total(const Context& ctx, const float* logits_dev, const float* y_dev, const Shape& shape,
+                             const LossConfig& cfg, uint64_t seed, double* grad_dev = nullptr,
+                             void* stream = nullptr) {
+    const pkv_loss_config c = cfg.c();
+    LossReport r{};
+    check(pkv_loss_total(ctx.get(), logits_dev, y_dev, shape.data(), static_cast<int>(shape.size()), &c, seed, &r,
+                         grad_dev, stream));
+    return r;
+}
+
 }  // namespace proxykv_b200

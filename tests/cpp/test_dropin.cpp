@@ -50,6 +50,10 @@ int main() {
     bad.stride = 128;
     CHECK(throws<ValueError>([&] { mapper_init_params(g, bad, 0); }));
     CHECK(mapper_init_params(g, MapperConfig{}, 1).size() > 15000000);
+    // loss.hpp:16-31 defaults carried into the C struct
+    const LossConfig lcfg;  // c() points into lcfg.ratios: keep lcfg alive while lc is used
+    const pkv_loss_config lc = lcfg.c();
+    CHECK(lc.n_ratios == 7 && lc.ratios[0] == 0.05 && lc.max_pairs == 4096 && lc.lambda_mse == 20.0);
 
     if (pkv_sm100_device_count() == 0) {
         CHECK(throws<NoDeviceError>([] { Context c(0); }));
