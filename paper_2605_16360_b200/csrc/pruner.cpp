@@ -30,11 +30,15 @@ struct pkv_pruner_s {
     cudaEvent_t ev = nullptr;
     // host-buffer form: copy stream + events (proxy layer chunks, target KV)
     cudaStream_t copy_st = nullptr;
-    static constexpr int kChunks = 4;
+    static constexpr int kChunks = 16;  // proxy-layer chunks of the H2D
+    static constexpr int kGroups = 4;   // target-layer groups of the map -> select -> compact -> D2H tail
     cudaEvent_t ev_in[kChunks + 2] = {};
+    cudaEvent_t ev_grp[kGroups + 1] = {};
     ~pkv_pruner_s() {
         if (ev) cudaEventDestroy(ev);
         for (cudaEvent_t e : ev_in)
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : ev_grp)
             if (e) cudaEventDestroy(e);
         if (copy_st) cudaStreamDestroy(copy_st);
     }
@@ -50,7 +54,58 @@ struct HostArrival {
     int64_t chunk_layers = 0;
     const cudaEvent_t* ev_chunk = nullptr;
     cudaEvent_t ev_kv = nullptr;
+    // outputs leaving for the host: when set (layer mode), the tail runs per
+    // target-layer group and each group's packed K/V + indices are copied out
+    // on `copy` while the next group is mapped
+    void* k_out_h = nullptr;
+    void* v_out_h = nullptr;
+    int32_t* idx_out_h = nullptr;
+    cudaStream_t copy = nullptr;
+    const cudaEvent_t* ev_grp = nullptr;  // kGroups + 1
 };
+
+// map -> select -> compact per group of target layers (contiguous unit
+// blocks, so no unit is mapped twice), each group's outputs D2H on arr.copy
+// while the next group is mapped; `ps` finally waits for the last copy.
+void grouped_tail(pkv_pruner p, const float* x, const void* kt, const void* vt, void* k_out, void* v_out,
+                  int32_t* idx, float* y, cudaStream_t ps, const HostArrival& arr) {
+    const int64_t units = static_cast<int64_t>(p->unit_off.size());
+    const int64_t nt = static_cast<int64_t>(p->out_unit.size());
+    const int G = static_cast<int>(std::min<int64_t>(pkv_pruner_s::kGroups, units));
+    const size_t row_kv = static_cast<size_t>(p->N * p->dt) * 2, row_out = static_cast<size_t>(p->K * p->dt) * 2;
+    int64_t t0 = 0;
+    for (int g = 0; g < G; ++g) {
+        const int64_t u0 = units * g / G, u1 = units * (g + 1) / G;
+        int64_t t1 = t0;
+        while (t1 < nt && p->out_unit[t1] < u1) ++t1;
+        if (t1 == t0) continue;
+        std::vector<int64_t> uo(p->unit_off.begin() + u0, p->unit_off.begin() + u1);
+        std::vector<int> ou(p->out_unit.begin() + t0, p->out_unit.begin() + t1);
+        for (int& v : ou) v -= static_cast<int>(u0);
+        p->mapper->run(x, uo, p->N, ou, y + t0 * p->Hl * p->N, ps);
+        if (g == 0) PKV_CUDA(cudaStreamWaitEvent(ps, arr.ev_kv, 0));
+        const int64_t s0 = t0 * p->Hl, ns = (t1 - t0) * p->Hl;
+        launch_topk_select(y + s0 * p->N, ns, p->N, p->K, nullptr, idx + s0 * p->K, ps);
+        launch_compact_kv(static_cast<const uint8_t*>(kt) + s0 * row_kv, static_cast<const uint8_t*>(vt) + s0 * row_kv,
+                          idx + s0 * p->K, ns, p->N, p->K, p->dt * 2, static_cast<uint8_t*>(k_out) + s0 * row_out,
+                          static_cast<uint8_t*>(v_out) + s0 * row_out, p->ctx->sm_count, ps);
+        count_launch(p->ctx, 2);
+        PKV_CUDA(cudaEventRecord(arr.ev_grp[g], ps));
+        PKV_CUDA(cudaStreamWaitEvent(arr.copy, arr.ev_grp[g], 0));
+        PKV_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(arr.k_out_h) + s0 * row_out,
+                                 static_cast<uint8_t*>(k_out) + s0 * row_out, ns * row_out, cudaMemcpyDeviceToHost,
+                                 arr.copy));
+        PKV_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(arr.v_out_h) + s0 * row_out,
+                                 static_cast<uint8_t*>(v_out) + s0 * row_out, ns * row_out, cudaMemcpyDeviceToHost,
+                                 arr.copy));
+        if (arr.idx_out_h)
+            PKV_CUDA(cudaMemcpyAsync(arr.idx_out_h + s0 * p->K, idx + s0 * p->K, ns * p->K * 4,
+                                     cudaMemcpyDeviceToHost, arr.copy));
+        t0 = t1;
+    }
+    PKV_CUDA(cudaEventRecord(arr.ev_grp[pkv_pruner_s::kGroups], arr.copy));
+    PKV_CUDA(cudaStreamWaitEvent(ps, arr.ev_grp[pkv_pruner_s::kGroups], 0));
+}
 
 pkv_pruner make_pruner(pkv_ctx ctx, pkv_mapper m, int64_t Hq, int64_t dp, int64_t dt, int64_t N, double rho,
                        uint32_t score_flags, uint32_t mode, int world, int rank, pkv_comm comm) {
@@ -134,6 +189,12 @@ void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, con
                 count_launch(p->ctx, 2);
             }
         }
+        // (2)-(4) per target-layer group with the outputs leaving for the host
+        if (arr && arr->k_out_h && pl.mode != PKV_SHARD_HEAD && ts == ps && slices > 0 &&
+            n_map * p->Hl == slices) {
+            grouped_tail(p, x, kt, vt, k_out, v_out, idx, y_sel, ps, *arr);
+            return;
+        }
         // (2) mapper: Ŷ for target layers [a, b), all heads
         p->mapper->run(x, p->unit_off, p->N, p->out_unit, y_map, ps);
     }
@@ -210,6 +271,7 @@ pkv_status pkv_pruner_run_host(pkv_pruner p, const void* q_h, const void* kp_h, 
         if (!p->copy_st) {
             PKV_CUDA(cudaStreamCreateWithFlags(&p->copy_st, cudaStreamNonBlocking));
             for (cudaEvent_t& e : p->ev_in) PKV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            for (cudaEvent_t& e : p->ev_grp) PKV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         }
         cudaStream_t cs = p->copy_st;
         constexpr int kC = pkv_pruner_s::kChunks;
@@ -239,11 +301,23 @@ pkv_status pkv_pruner_run_host(pkv_pruner p, const void* q_h, const void* kp_h, 
         PKV_CUDA(cudaMemcpyAsync(in + qb + kpb + kvb, vt_h, kvb, cudaMemcpyHostToDevice, cs));
         PKV_CUDA(cudaEventRecord(p->ev_in[kC], cs));
         arr.ev_kv = p->ev_in[kC];
+        // layer mode: the outputs leave per target-layer group (grouped_tail)
+        const bool grouped = pl.mode != PKV_SHARD_HEAD && pl.b > pl.a && p->slices() > 0 &&
+                             (pl.b - pl.a) * p->Hl == p->slices();
+        if (grouped) {
+            arr.k_out_h = k_out_h;
+            arr.v_out_h = v_out_h;
+            arr.idx_out_h = idx_out_h;
+            arr.copy = cs;
+            arr.ev_grp = p->ev_grp;
+        }
         run_pruner(p, in, in + qb, in + qb + kpb, in + qb + kpb + kvb, outb, outb + ob,
                    reinterpret_cast<int32_t*>(outb + 2 * ob), nullptr, st, st, &arr);
-        PKV_CUDA(cudaMemcpyAsync(k_out_h, outb, ob, cudaMemcpyDeviceToHost, st));
-        PKV_CUDA(cudaMemcpyAsync(v_out_h, outb + ob, ob, cudaMemcpyDeviceToHost, st));
-        if (idx_out_h) PKV_CUDA(cudaMemcpyAsync(idx_out_h, outb + 2 * ob, ib, cudaMemcpyDeviceToHost, st));
+        if (!grouped) {
+            PKV_CUDA(cudaMemcpyAsync(k_out_h, outb, ob, cudaMemcpyDeviceToHost, st));
+            PKV_CUDA(cudaMemcpyAsync(v_out_h, outb + ob, ob, cudaMemcpyDeviceToHost, st));
+            if (idx_out_h) PKV_CUDA(cudaMemcpyAsync(idx_out_h, outb + 2 * ob, ib, cudaMemcpyDeviceToHost, st));
+        }
         PKV_CUDA(cudaStreamSynchronize(st));
     });
 }

@@ -119,3 +119,35 @@ def test_pruner_deterministic(tiny):
         outs.append((y.clone(), idx.clone()))
     torch.cuda.synchronize()
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("Ls,Ll,Hl", [(5, 7, 2), (16, 32, 2), (3, 3, 4)])
+def test_pruner_host_grouped_tail_matches_device(gpu, Ls, Ll, Hl):
+    """pkv_pruner_run_host maps / selects / compacts per target-layer group and
+    copies each group out while the next is mapped; the result must equal the
+    device-resident run bit for bit, for unit counts that do not split evenly
+    into the groups and pairings that are not 2:1."""
+    import torch
+    import paper_2605_16360_b200 as P
+    Hq, Hs, dp, dt, N, rho = 4, 2, 64, 64, 1024, 0.3
+    geom = P.ModelGeometry(Ll, Hl, Ls, Hs, dt)
+    m = P.Mapper(geom, P.MapperConfig(encoder_layers=1), seed=3, ctx=gpu)
+    pr = P.Pruner(m, Hq, dp, dt, N, rho)
+    K = pr.k
+    r = np.random.RandomState(Ls * 100 + Ll)
+    bf = lambda a: torch.from_numpy(O.f32_to_bf16_bits(a.astype(np.float32)).view(np.int16)).view(torch.bfloat16)
+    q = bf(r.standard_normal((Ls, Hq, N, dp)) * 0.35).pin_memory()
+    kp = bf(r.standard_normal((Ls, Hs, N, dp))).pin_memory()
+    kt = torch.from_numpy(r.randint(0, 1 << 15, (Ll, Hl, N, dt)).astype(np.int16)).view(torch.bfloat16).pin_memory()
+    vt = torch.from_numpy(r.randint(0, 1 << 15, (Ll, Hl, N, dt)).astype(np.int16)).view(torch.bfloat16).pin_memory()
+    ko = torch.empty(Ll, Hl, K, dt, dtype=torch.bfloat16).pin_memory()
+    vo = torch.empty_like(ko).pin_memory()
+    idx = torch.empty(Ll, Hl, K, dtype=torch.int32).pin_memory()
+    pr.run_host(q, kp, kt, vt, ko, vo, idx)
+    dko = torch.empty(Ll, Hl, K, dt, dtype=torch.bfloat16, device="cuda")
+    dvo = torch.empty_like(dko)
+    didx = torch.empty(Ll, Hl, K, dtype=torch.int32, device="cuda")
+    pr.run(q.cuda(), kp.cuda(), kt.cuda(), vt.cuda(), dko, dvo, didx)
+    torch.cuda.synchronize()
+    assert torch.equal(idx, didx.cpu())
+    assert torch.equal(_t(ko), _t(dko.cpu())) and torch.equal(_t(vo), _t(dvo.cpu()))
