@@ -147,6 +147,14 @@ pkv_status pkv_compact_kv(pkv_ctx ctx, const void* k_in_dev, const void* v_in_de
                           int64_t slices, int64_t n, int64_t k, int64_t d, int64_t elem_bytes, void* k_out_dev,
                           void* v_out_dev, void* stream);
 
+/* The same gather into a paged cache: row j of slice
+ * s goes to page block_table[s * max_blocks + j / page_size], row
+ * j % page_size, of the pools k_pool / v_pool [pages, page_size, d]. */
+pkv_status pkv_compact_kv_paged(pkv_ctx ctx, const void* k_in_dev, const void* v_in_dev, const int32_t* idx_asc_dev,
+                                int64_t slices, int64_t n, int64_t k, int64_t d, int64_t elem_bytes,
+                                const int32_t* block_table_dev, int64_t max_blocks, int64_t page_size,
+                                void* k_pool_dev, void* v_pool_dev, void* stream);
+
 /* ------------------------------------------------------ scoring (a-1) ---- */
 #define PKV_SCORE_REDUCE_MAX 0u /* north star: max over queries (and GQA group) */
 #define PKV_SCORE_REDUCE_SUM 1u /* SPEC.md:423-431 accumulate_attention / PAPER.md:46 */
@@ -265,6 +273,17 @@ pkv_status pkv_pruner_run_dual(pkv_pruner p, const void* q_dev, const void* kp_d
 pkv_status pkv_packed_decode_attention(pkv_ctx ctx, const void* q_dev, const void* k_packed_dev,
                                        const void* v_packed_dev, int64_t L, int64_t Hq, int64_t Hkv, int64_t K,
                                        int64_t d, double scale, float* out_dev, void* stream);
+
+/* Decode over a paged pruned cache with per-(layer, KV head) lengths: slab
+ * s = l * Hkv + kh holds seq_lens[s] rows, row r in page
+ * block_table[s * max_blocks + r / page_size] at row r % page_size of the
+ * bf16 pools [pages, page_size, d]; max_len >= every seq_lens[s] sizes the
+ * split-K grid. A slab of length 0 decodes to 0. Same kernel as the packed
+ * form with the row address taken through the block table. */
+pkv_status pkv_paged_decode_attention(pkv_ctx ctx, const void* q_dev, const void* k_pool_dev, const void* v_pool_dev,
+                                      const int32_t* block_table_dev, const int32_t* seq_lens_dev, int64_t L,
+                                      int64_t Hq, int64_t Hkv, int64_t max_blocks, int64_t page_size, int64_t max_len,
+                                      int64_t d, double scale, float* out_dev, void* stream);
 
 /* ------------------------------------------- file formats -- */
 /* Host-only. Little-endian, binio.hpp semantics; corrupt files return the

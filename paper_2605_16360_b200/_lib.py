@@ -82,6 +82,10 @@ SIGNATURES = {
     "pkv_topk_mask_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_dbl, _c_vp, _c_i64p]),
     "pkv_topk_overlap": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp]),
     "pkv_captured_mass": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp]),
+    "pkv_compact_kv_paged": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_vp,
+                                            _c_i64, _c_i64, _c_vp, _c_vp, _c_vp]),
+    "pkv_paged_decode_attention": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64,
+                                                  _c_i64, _c_i64, _c_i64, _c_i64, ctypes.c_double, _c_vp, _c_vp]),
     "pkv_spearman": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_vp, _c_vp]),
     "pkv_loss_total": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp, ctypes.c_int, _c_vp, ctypes.c_uint64, _c_vp, _c_vp,
                                       _c_vp]),

@@ -192,6 +192,26 @@ pkv_status pkv_compact_kv(pkv_ctx ctx, const void* k_in_dev, const void* v_in_de
     });
 }
 
+pkv_status pkv_compact_kv_paged(pkv_ctx ctx, const void* k_in_dev, const void* v_in_dev, const int32_t* idx_asc_dev,
+                                int64_t slices, int64_t n, int64_t k, int64_t d, int64_t elem_bytes,
+                                const int32_t* block_table_dev, int64_t max_blocks, int64_t page_size,
+                                void* k_pool_dev, void* v_pool_dev, void* stream) {
+    return guard([&] {
+        require_ctx(ctx);
+        PKV_REQUIRE_SHAPE(slices >= 0 && n > 0 && d > 0, "compact_kv extents must be positive");
+        PKV_REQUIRE_VALUE(k >= 1 && k <= n, "top-k count ", k, " out of range for length ", n);
+        PKV_REQUIRE_VALUE(elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4, "elem_bytes must be 1, 2 or 4");
+        PKV_REQUIRE_VALUE((d * elem_bytes) % 2 == 0, "row bytes must be even");
+        PKV_REQUIRE_VALUE(block_table_dev != nullptr && page_size > 0, "paged compaction needs a block table");
+        PKV_REQUIRE_VALUE(max_blocks * page_size >= k, "block table too short: ", max_blocks, " pages of ",
+                          page_size, " rows < k = ", k);
+        launch_compact_kv_paged(k_in_dev, v_in_dev, idx_asc_dev, slices, n, k, d * elem_bytes, k_pool_dev,
+                                v_pool_dev, block_table_dev, max_blocks, page_size, ctx->sm_count,
+                                static_cast<cudaStream_t>(stream));
+        count_launch(ctx);
+    });
+}
+
 }  // extern "C"
 
 // ------------------------------------------------------------- scoring ----

@@ -41,13 +41,22 @@ using sm100::ffma2;
 using sm100::pack2;
 using sm100::unpack2;
 
+// Paged cache (vLLM-style): row r of (layer, KV head) slab s lives in page
+// table[s·max_blocks + r / page] at row r % page of the [pages, page, D] pools;
+// slab s holds lens[s] rows (per-head variable length).
+struct Paged {
+    const int32_t* table = nullptr;
+    const int32_t* lens = nullptr;
+    int64_t max_blocks = 0, page = 0;
+};
+
 // partial: [L, Hq, splits] x {m (log2 domain), l, o[D]}. G: group-size
 // bucket (1, 2, 4, 8); g <= G heads are live (g = 7 for Qwen-2.5-7B).
-template <int D, int G>
+template <int D, int G, bool kPaged>
 __global__ void __launch_bounds__(32 * kWarps)
     decode_split_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kc,
                         const __nv_bfloat16* __restrict__ vc, int Hq, int Hkv, int g, int64_t K, int64_t chunk,
-                        float scale_log2, float* __restrict__ part) {
+                        float scale_log2, float* __restrict__ part, Paged pg) {
     // lanes per key row: 8 (16 dims each at d = 128), 16 for G = 8 at d = 128 (register budget)
     constexpr int kLPK = (G >= 8 && D == 128) ? 16 : 8;
     constexpr int kKPW = 32 / kLPK;  // keys per warp step
@@ -56,10 +65,12 @@ __global__ void __launch_bounds__(32 * kWarps)
     const int splits = gridDim.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / kLPK, sub = lane % kLPK;  // key group, lane within the group
-    const int64_t k_lo = split * chunk, k_hi = min(K, k_lo + chunk);
     const int64_t kslab = (int64_t)l * Hkv + kh;
-    const __nv_bfloat16* kbase = kc + kslab * K * D + sub * kDL;
-    const __nv_bfloat16* vbase = vc + kslab * K * D + sub * kDL;
+    const int64_t len = kPaged ? (int64_t)__ldg(pg.lens + kslab) : K;
+    const int64_t k_lo = split * chunk, k_hi = min(len, k_lo + chunk);
+    const __nv_bfloat16* kbase = kPaged ? kc + sub * kDL : kc + kslab * K * D + sub * kDL;
+    const __nv_bfloat16* vbase = kPaged ? vc + sub * kDL : vc + kslab * K * D + sub * kDL;
+    const int32_t* ptab = kPaged ? pg.table + kslab * pg.max_blocks : nullptr;
 
     // this lane's slice of the group's queries (pre-scaled to the log2 domain)
     float qr[G][kDL];
@@ -92,7 +103,8 @@ __global__ void __launch_bounds__(32 * kWarps)
     uint4 kraw[kV], vraw[kV], knx[kV], vnx[kV];
     auto load_row = [&](int64_t key0, uint4 (&kr)[kV], uint4 (&vr)[kV]) {
         const int64_t key = key0 + grp;
-        const int64_t kk = key < k_hi ? key : k_lo;
+        int64_t kk = key < k_hi ? key : k_lo;
+        if (kPaged) kk = (int64_t)__ldg(ptab + kk / pg.page) * pg.page + kk % pg.page;  // pool row
 #pragma unroll
         for (int c = 0; c < kV; ++c) {
             kr[c] = __ldcs(reinterpret_cast<const uint4*>(kbase + kk * D + 8 * c));
@@ -213,7 +225,7 @@ __global__ void decode_merge_kernel(const float* __restrict__ part, int splits, 
 
 template <int D, int G>
 void run_decode(const DecodeShape& s, const void* q, const void* kc, const void* vc, float* out, DevBuf& ws,
-                int sm_count, cudaStream_t st) {
+                int sm_count, cudaStream_t st, const Paged& pg) {
     const int64_t heads = s.L * s.Hkv;
     // ~2 waves of CTAs (more splits cost more in per-CTA setup and the merge
     // than a partial last wave), at least 64 keys per split
@@ -223,10 +235,10 @@ void run_decode(const DecodeShape& s, const void* q, const void* kc, const void*
     splits = (s.K + chunk - 1) / chunk;
     float* part = static_cast<float*>(ws.get(static_cast<size_t>(s.L * s.Hq * splits * (2 + D)) * 4));
     const dim3 grid((unsigned)splits, (unsigned)s.Hkv, (unsigned)s.L);
-    decode_split_kernel<D, G><<<grid, 32 * kWarps, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(kc),
-        static_cast<const __nv_bfloat16*>(vc), (int)s.Hq, (int)s.Hkv, (int)(s.Hq / s.Hkv), s.K, chunk,
-        s.scale * 1.4426950408889634f, part);
+    auto kern = pg.table ? decode_split_kernel<D, G, true> : decode_split_kernel<D, G, false>;
+    kern<<<grid, 32 * kWarps, 0, st>>>(static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(kc),
+                                       static_cast<const __nv_bfloat16*>(vc), (int)s.Hq, (int)s.Hkv,
+                                       (int)(s.Hq / s.Hkv), s.K, chunk, s.scale * 1.4426950408889634f, part, pg);
     check_launch("decode_split_kernel");
     decode_merge_kernel<D><<<(unsigned)(s.L * s.Hq), D, 0, st>>>(part, (int)splits, out);
     check_launch("decode_merge_kernel");
@@ -234,20 +246,20 @@ void run_decode(const DecodeShape& s, const void* q, const void* kc, const void*
 
 template <int D>
 void dispatch_g(const DecodeShape& s, const void* q, const void* kc, const void* vc, float* out, DevBuf& ws, int sm,
-                cudaStream_t st) {
+                cudaStream_t st, const Paged& pg) {
     const int64_t g = s.Hq / s.Hkv;
-    if (g <= 1) return run_decode<D, 1>(s, q, kc, vc, out, ws, sm, st);
-    if (g <= 2) return run_decode<D, 2>(s, q, kc, vc, out, ws, sm, st);
-    if (g <= 4) return run_decode<D, 4>(s, q, kc, vc, out, ws, sm, st);
-    return run_decode<D, 8>(s, q, kc, vc, out, ws, sm, st);
+    if (g <= 1) return run_decode<D, 1>(s, q, kc, vc, out, ws, sm, st, pg);
+    if (g <= 2) return run_decode<D, 2>(s, q, kc, vc, out, ws, sm, st, pg);
+    if (g <= 4) return run_decode<D, 4>(s, q, kc, vc, out, ws, sm, st, pg);
+    return run_decode<D, 8>(s, q, kc, vc, out, ws, sm, st, pg);
 }
 
 }  // namespace
 
 void launch_packed_decode(const DecodeShape& s, const void* q, const void* kc, const void* vc, float* out, DevBuf& ws,
                           int sm_count, cudaStream_t st) {
-    if (s.d == 128) dispatch_g<128>(s, q, kc, vc, out, ws, sm_count, st);
-    else dispatch_g<64>(s, q, kc, vc, out, ws, sm_count, st);
+    if (s.d == 128) dispatch_g<128>(s, q, kc, vc, out, ws, sm_count, st, Paged{});
+    else dispatch_g<64>(s, q, kc, vc, out, ws, sm_count, st, Paged{});
 }
 
 }  // namespace pkv
@@ -267,6 +279,30 @@ extern "C" pkv_status pkv_packed_decode_attention(pkv_ctx ctx, const void* q_dev
         DecodeShape s{L, Hq, Hkv, K, d, static_cast<float>(scale)};
         launch_packed_decode(s, q_dev, k_packed_dev, v_packed_dev, out_dev, ctx->scratch_decode, ctx->sm_count,
                              static_cast<cudaStream_t>(stream));
+        count_launch(ctx, 2);
+    });
+}
+
+extern "C" pkv_status pkv_paged_decode_attention(pkv_ctx ctx, const void* q_dev, const void* k_pool_dev,
+                                                 const void* v_pool_dev, const int32_t* block_table_dev,
+                                                 const int32_t* seq_lens_dev, int64_t L, int64_t Hq, int64_t Hkv,
+                                                 int64_t max_blocks, int64_t page_size, int64_t max_len, int64_t d,
+                                                 double scale, float* out_dev, void* stream) {
+    return guard([&] {
+        require_ctx(ctx);
+        PKV_REQUIRE_SHAPE(L > 0 && Hq > 0 && Hkv > 0 && max_len > 0, "paged decode extents must be positive");
+        PKV_REQUIRE_SHAPE(Hq % Hkv == 0, "query heads ", Hq, " not a multiple of KV heads ", Hkv);
+        PKV_REQUIRE_VALUE(block_table_dev && seq_lens_dev && page_size > 0, "paged decode needs a block table");
+        PKV_REQUIRE_VALUE(max_blocks * page_size >= max_len, "block table too short for max_len ", max_len);
+        PKV_REQUIRE(d == 64 || d == 128, PKV_ECONFIG, "paged decode supports head_dim 64 or 128, got ", d);
+        PKV_REQUIRE(Hq / Hkv <= kMaxG, PKV_ECONFIG, "paged decode supports GQA groups up to ", kMaxG);
+        PKV_REQUIRE(L * Hkv <= 65535, PKV_ECONFIG, "too many (layer, KV head) pairs for one launch");
+        // splits sized on max_len; slabs shorter than a split's start contribute nothing
+        DecodeShape s{L, Hq, Hkv, max_len, d, static_cast<float>(scale)};
+        const Paged pg{block_table_dev, seq_lens_dev, max_blocks, page_size};
+        auto st = static_cast<cudaStream_t>(stream);
+        if (d == 128) dispatch_g<128>(s, q_dev, k_pool_dev, v_pool_dev, out_dev, ctx->scratch_decode, ctx->sm_count, st, pg);
+        else dispatch_g<64>(s, q_dev, k_pool_dev, v_pool_dev, out_dev, ctx->scratch_decode, ctx->sm_count, st, pg);
         count_launch(ctx, 2);
     });
 }

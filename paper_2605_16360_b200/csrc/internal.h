@@ -92,6 +92,10 @@ void launch_topk_select(const float* scores, int64_t slices, int64_t n, int64_t 
                         cudaStream_t st);
 void launch_compact_kv(const void* kin, const void* vin, const int32_t* idx, int64_t slices, int64_t n, int64_t k,
                        int64_t row_bytes, void* kout, void* vout, int sm_count, cudaStream_t st);
+// paged destination: slice s's output row j -> page table[s * max_blocks + j / page], row j % page
+void launch_compact_kv_paged(const void* kin, const void* vin, const int32_t* idx, int64_t slices, int64_t n,
+                             int64_t k, int64_t row_bytes, void* k_pool, void* v_pool, const int32_t* table,
+                             int64_t max_blocks, int64_t page, int sm_count, cudaStream_t st);
 
 // TMA descriptor encoding through the driver entry point (no -lcuda needed).
 CUtensorMap make_tmap_2d(const void* base, CUtensorMapDataType dt, uint64_t inner, uint64_t outer,

@@ -23,7 +23,7 @@ from ._lib import (BadMagicError, ConfigError, CudaError, IoError, NoDeviceError
 __all__ = [
     "Context", "PruneMask", "MaskApplication", "ModelGeometry", "MapperConfig", "Mapper", "Pruner",
     "retention_count", "topk_select", "topk_mask", "apply_mask", "compact_kv", "score", "score_lse",
-    "proxy_prefill_attention", "packed_decode_attention", "topk_overlap_device", "captured_mass_device",
+    "proxy_prefill_attention", "packed_decode_attention", "paged_decode_attention", "compact_kv_paged", "topk_overlap_device", "captured_mass_device",
     "spearman_device", "slice_metrics_device", "MetricAccumulator", "MetricReport",
     "LossConfig", "LossReport", "loss_total",
     "layer_pair", "window_offsets", "mapper_init_params", "ShapeError", "PkvValueError", "ConfigError",
@@ -414,6 +414,36 @@ def packed_decode_attention(q, k_packed, v_packed, *, scale: float = None, ctx: 
     check(lib().pkv_packed_decode_attention(ctx.h, _ptr(q), _ptr(k_packed), _ptr(v_packed), L, hq, hkv, K, d, sc,
                                             _ptr(o), _stream(stream)))
     return o
+
+
+def paged_decode_attention(q, k_pool, v_pool, block_table, seq_lens, *, max_len: int = None, scale: float = None,
+                           ctx: Context = None, stream=None, out=None):
+    """Decode over a paged cache: q bf16 [L, Hq, d]; k/v_pool bf16 [pages, page, d];
+    block_table i32 [L, Hkv, max_blocks]; seq_lens i32 [L, Hkv] -> fp32 [L, Hq, d]."""
+    torch = _torch()
+    ctx = ctx or Context.default(q.device.index or 0)
+    L, hq, d = q.shape
+    _, hkv, mb = block_table.shape
+    page = k_pool.shape[1]
+    ml = int(max_len) if max_len is not None else int(seq_lens.max().item())
+    o = out if out is not None else torch.empty((L, hq, d), dtype=torch.float32, device=q.device)
+    sc = float(scale) if scale is not None else 1.0 / d ** 0.5
+    check(lib().pkv_paged_decode_attention(ctx.h, _ptr(q), _ptr(k_pool), _ptr(v_pool), _ptr(block_table.contiguous()),
+                                           _ptr(seq_lens.contiguous()), L, hq, hkv, mb, page, max(ml, 1), d, sc,
+                                           _ptr(o), _stream(stream)))
+    return o
+
+
+def compact_kv_paged(k_in, v_in, idx_asc, block_table, k_pool, v_pool, *, ctx: Context = None, stream=None):
+    """Gather retained rows into pages: k_in/v_in [S, n, d] (2-byte) cuda, idx_asc
+    i32 [S, k], block_table i32 [S, max_blocks], pools [pages, page, d]."""
+    ctx = ctx or Context.default(k_in.device.index or 0)
+    S, n, d = k_in.shape
+    k = idx_asc.shape[1]
+    check(lib().pkv_compact_kv_paged(ctx.h, _ptr(k_in), _ptr(v_in), _ptr(idx_asc), S, n, k, d, k_in.element_size(),
+                                     _ptr(block_table.contiguous()), block_table.shape[-1], k_pool.shape[1],
+                                     _ptr(k_pool), _ptr(v_pool), _stream(stream)))
+    return k_pool, v_pool
 
 
 def score_lse(q, k, *, causal: bool = False, ctx: Context = None, stream=None):
