@@ -18,6 +18,8 @@
 //   pass 2: merge the splits (log-sum-exp weighted) into o.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "decode.cuh"
 #include "sm100.cuh"
 
@@ -26,6 +28,7 @@ namespace {
 
 constexpr int kWarps = 8;
 constexpr int kMaxG = 8;
+constexpr float kLazy = 8.0f;  // log2 headroom before a group's running max is raised
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
@@ -53,12 +56,12 @@ struct Paged {
 // partial: [L, Hq, splits] x {m (log2 domain), l, o[D]}. G: group-size
 // bucket (1, 2, 4, 8); g <= G heads are live (g = 7 for Qwen-2.5-7B).
 template <int D, int G, bool kPaged>
-__global__ void __launch_bounds__(32 * kWarps)
+__global__ void __launch_bounds__(32 * kWarps, 2)
     decode_split_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kc,
                         const __nv_bfloat16* __restrict__ vc, int Hq, int Hkv, int g, int64_t K, int64_t chunk,
                         float scale_log2, float* __restrict__ part, Paged pg) {
     // lanes per key row: 8 (16 dims each at d = 128), 16 for G = 8 at d = 128 (register budget)
-    constexpr int kLPK = (G >= 8 && D == 128) ? 16 : 8;
+    constexpr int kLPK = (G >= 4 && D == 128) ? 16 : 8;
     constexpr int kKPW = 32 / kLPK;  // keys per warp step
     constexpr int kDL = D / kLPK;    // dims per lane
     const int split = blockIdx.x, kh = blockIdx.y, l = blockIdx.z;
@@ -128,30 +131,49 @@ __global__ void __launch_bounds__(32 * kWarps)
 #pragma unroll
             for (int e = 0; e < 8; ++e) vf[8 * c + e] = f[e];
         }
+        // all G dots first, then the G butterfly reductions interleaved step by
+        // step (independent shuffle chains), then the online-softmax updates
+        float sc[G];
 #pragma unroll
         for (int h = 0; h < G; ++h) {
-            if (h >= g) break;  // warp-uniform
-            // dot as packed FFMA2 over dimension pairs, then the group reduction
             uint64_t s2 = pack2(0.0f, 0.0f);
 #pragma unroll
             for (int e = 0; e < kDL; e += 2) s2 = ffma2(pack2(qr[h][e], qr[h][e + 1]), pack2(kf[e], kf[e + 1]), s2);
             const float2 sp = unpack2(s2);
-            float s = sp.x + sp.y;
+            sc[h] = sp.x + sp.y;
+        }
 #pragma unroll
-            for (int o2 = 1; o2 < kLPK; o2 <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o2);
-            if (ok) {
-                const float mn = fmaxf(m[h], s);
-                const float a = ex2(m[h] - mn), p = ex2(s - mn);  // ex2(-inf) = 0
-                ls[h] = ls[h] * a + p;
-                const uint64_t aa = pack2(a, a), pp = pack2(p, p);
+        for (int o2 = 1; o2 < kLPK; o2 <<= 1)
+#pragma unroll
+            for (int h = 0; h < G; ++h) sc[h] += __shfl_xor_sync(0xffffffffu, sc[h], o2);
+        if (ok) {
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+                if (h >= g) break;  // warp-uniform
+                const float s = sc[h];
+                // lazy rescale: the reference max moves only when a score
+                // exceeds it by more than 2^kLazy (p <= 2^8 is exact in fp32)
+                if (s > m[h] + kLazy) {
+                    const float a = ex2(m[h] - s);  // 0 on the first key (m = -inf)
+                    ls[h] *= a;
+                    const uint64_t aa = pack2(a, a);
+#pragma unroll
+                    for (int e = 0; e < kDL; e += 2) {
+                        const float2 r = unpack2(sm100::fmul2(pack2(o[h][e], o[h][e + 1]), aa));
+                        o[h][e] = r.x;
+                        o[h][e + 1] = r.y;
+                    }
+                    m[h] = s;
+                }
+                const float p = ex2(s - m[h]);
+                ls[h] += p;
+                const uint64_t pp = pack2(p, p);
 #pragma unroll
                 for (int e = 0; e < kDL; e += 2) {
-                    const uint64_t oe = sm100::fmul2(pack2(o[h][e], o[h][e + 1]), aa);
-                    const float2 r = unpack2(ffma2(pp, pack2(vf[e], vf[e + 1]), oe));
+                    const float2 r = unpack2(ffma2(pp, pack2(vf[e], vf[e + 1]), pack2(o[h][e], o[h][e + 1])));
                     o[h][e] = r.x;
                     o[h][e + 1] = r.y;
                 }
-                m[h] = mn;
             }
         }
 #pragma unroll
