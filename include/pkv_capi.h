@@ -264,6 +264,17 @@ pkv_status pkv_pruner_run_dual(pkv_pruner p, const void* q_dev, const void* kp_d
                                const void* vt_dev, void* k_out_dev, void* v_out_dev, int32_t* idx_out_dev,
                                float* scores_out_dev, void* proxy_stream, void* target_stream);
 
+/* Two-device proxy -> target: the pruner's
+ * context device scores and maps (q, kp on it; proxy_stream there); the mapped
+ * scores cross with one peer copy; select + compaction run on target_ctx's
+ * device on target_stream (kt/vt/outputs live there), gated by an event.
+ * scores_target_dev (nullable) receives Ŷ on the target device. Unsharded
+ * pruners only. Outputs are identical to pkv_pruner_run's. */
+pkv_status pkv_pruner_run_two_device(pkv_pruner p, pkv_ctx target_ctx, const void* q_dev, const void* kp_dev,
+                                     const void* kt_target_dev, const void* vt_target_dev, void* k_out_target_dev,
+                                     void* v_out_target_dev, int32_t* idx_out_target_dev, float* scores_target_dev,
+                                     void* proxy_stream, void* target_stream);
+
 /* Target-side consumption of the packed cache: one
  * decode query per query head over its KV head's retained rows,
  *   out[l,h,:] = softmax(q[l,h]·K_packed[l,h/g]^T · scale) · V_packed[l,h/g]

@@ -26,6 +26,8 @@ struct pkv_pruner_s {
     std::vector<int64_t> unit_off;  // mapper units (unique proxy layers of target layers [a, b))
     std::vector<int> out_unit;      // target layer a + i -> unit
     DevBuf lam, x, y, y_local, idx;
+    DevBuf y_remote;  // two-device mode: Ŷ on the target device (allocated there)
+    cudaEvent_t ev_remote = nullptr;
     DevBuf host_in, host_out;  // device copies for the host-buffer form
     cudaEvent_t ev = nullptr;
     // host-buffer form: copy stream + events (proxy layer chunks, target KV)
@@ -36,6 +38,7 @@ struct pkv_pruner_s {
     cudaEvent_t ev_grp[kGroups + 1] = {};
     ~pkv_pruner_s() {
         if (ev) cudaEventDestroy(ev);
+        if (ev_remote) cudaEventDestroy(ev_remote);
         for (cudaEvent_t e : ev_in)
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : ev_grp)
@@ -250,6 +253,56 @@ pkv_status pkv_pruner_run_dual(pkv_pruner p, const void* q, const void* kp, cons
         PKV_REQUIRE_VALUE(p != nullptr, "null pkv_pruner");
         run_pruner(p, q, kp, kt, vt, k_out, v_out, idx_out, scores_out, static_cast<cudaStream_t>(proxy_stream),
                    static_cast<cudaStream_t>(target_stream));
+    });
+}
+
+// Paper regime: the proxy device scores
+// and maps; Ŷ crosses to the target device with one peer copy on the proxy
+// stream, and the target stream (on the target device) waits for it before
+// select + compaction. Outputs are identical to pkv_pruner_run.
+pkv_status pkv_pruner_run_two_device(pkv_pruner p, pkv_ctx target_ctx, const void* q_dev, const void* kp_dev,
+                                     const void* kt_target_dev, const void* vt_target_dev, void* k_out_target_dev,
+                                     void* v_out_target_dev, int32_t* idx_out_target_dev, float* scores_target_dev,
+                                     void* proxy_stream, void* target_stream) {
+    return guard([&] {
+        PKV_REQUIRE_VALUE(p != nullptr, "null pkv_pruner");
+        require_ctx(target_ctx);
+        PKV_REQUIRE_VALUE(p->plan.world == 1, "two-device mode runs one whole context (world 1)");
+        auto ps = static_cast<cudaStream_t>(proxy_stream);
+        auto ts = static_cast<cudaStream_t>(target_stream);
+        const int dev_p = p->ctx->device, dev_t = target_ctx->device;
+        const int64_t slices = p->slices();
+        const size_t ybytes = static_cast<size_t>(slices * p->N) * 4;
+        PKV_CUDA(cudaSetDevice(dev_p));
+        // score -> map on the proxy device into p->y (no select: slices handled below)
+        float* y_p = static_cast<float*>(p->y.get(ybytes));
+        {
+            const ScoreShape& s = p->score;
+            auto* lam = static_cast<__nv_bfloat16*>(p->lam.get(static_cast<size_t>(s.L * s.Hq * s.Nq) * 16));
+            auto* x = static_cast<float*>(p->x.get(static_cast<size_t>(s.L * s.Hkv * s.Nk) * 4));
+            launch_score_lse(s, q_dev, kp_dev, nullptr, lam, ps);
+            launch_score_pool(s, q_dev, kp_dev, lam, p->reduce_max, x, ps);
+            count_launch(p->ctx, 2);
+            p->mapper->run(x, p->unit_off, p->N, p->out_unit, y_p, ps);
+        }
+        // Ŷ -> target device
+        PKV_CUDA(cudaSetDevice(dev_t));
+        float* y_t = scores_target_dev ? scores_target_dev : static_cast<float*>(p->y_remote.get(ybytes));
+        PKV_CUDA(cudaSetDevice(dev_p));
+        PKV_CUDA(cudaMemcpyPeerAsync(y_t, dev_t, y_p, dev_p, ybytes, ps));
+        if (!p->ev_remote) PKV_CUDA(cudaEventCreateWithFlags(&p->ev_remote, cudaEventDisableTiming));
+        PKV_CUDA(cudaEventRecord(p->ev_remote, ps));
+        // select + compaction on the target device
+        PKV_CUDA(cudaSetDevice(dev_t));
+        PKV_CUDA(cudaStreamWaitEvent(ts, p->ev_remote, 0));
+        int32_t* idx = idx_out_target_dev ? idx_out_target_dev
+                                          : static_cast<int32_t*>(target_ctx->scratch_select.get(
+                                                static_cast<size_t>(slices * p->K) * 4));
+        launch_topk_select(y_t, slices, p->N, p->K, nullptr, idx, ts);
+        launch_compact_kv(kt_target_dev, vt_target_dev, idx, slices, p->N, p->K, p->dt * 2, k_out_target_dev,
+                          v_out_target_dev, target_ctx->sm_count, ts);
+        count_launch(target_ctx, 2);
+        PKV_CUDA(cudaSetDevice(dev_p));
     });
 }
 

@@ -664,6 +664,14 @@ class Pruner:
                                         _ptr(idx_out), _ptr(scores_out), _stream(proxy_stream),
                                         _stream(target_stream)))
 
+    def run_two_device(self, target_ctx: "Context", q, kp, kt, vt, k_out, v_out, idx_out=None, scores_out=None, *,
+                       proxy_stream=None, target_stream=None):
+        """Paper regime: score + map on this pruner's device (q, kp there), Ŷ peer-copied to
+        target_ctx's device, select + compaction there (kt, vt, outputs there)."""
+        check(lib().pkv_pruner_run_two_device(self.h, target_ctx.h, _ptr(q), _ptr(kp), _ptr(kt), _ptr(vt),
+                                              _ptr(k_out), _ptr(v_out), _ptr(idx_out), _ptr(scores_out),
+                                              _stream(proxy_stream), _stream(target_stream)))
+
     def run_host(self, q, kp, kt, vt, k_out, v_out, idx_out=None, stream=None):
         """Host (ideally pinned) torch tensors in and out; copies happen inside the call."""
         check(lib().pkv_pruner_run_host(self.h, _ptr(q), _ptr(kp), _ptr(kt), _ptr(vt), _ptr(k_out), _ptr(v_out),

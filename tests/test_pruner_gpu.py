@@ -151,3 +151,36 @@ def test_pruner_host_grouped_tail_matches_device(gpu, Ls, Ll, Hl):
     torch.cuda.synchronize()
     assert torch.equal(idx, didx.cpu())
     assert torch.equal(_t(ko), _t(dko.cpu())) and torch.equal(_t(vo), _t(dvo.cpu()))
+
+
+def test_pruner_two_device_matches_single(tiny):
+    """pkv_pruner_run_two_device (proxy device -> peer copy of Ŷ -> target
+    device select + compaction) gives pkv_pruner_run's outputs. On one GPU
+    both contexts are device 0 (the peer copy is then a device copy); on a
+    multi-GPU box the target is device 1."""
+    import torch
+    P, pr = tiny["P"], tiny["pr"]
+    Ls, Hq, Hs, dp, Ll, Hl, dt, N, rho = tiny["dims"]
+    K = pr.k
+    tdev = 1 if torch.cuda.device_count() > 1 else 0
+    tctx = P.Context(tdev)
+    dev = lambda a, d=0: torch.from_numpy(a.view(np.int16)).to(f"cuda:{d}").view(torch.bfloat16)
+    q, kp = dev(tiny["qb"]), dev(tiny["kpb"])
+    kt, vt = dev(tiny["kt"], tdev), dev(tiny["vt"], tdev)
+    ko = torch.empty(Ll, Hl, K, dt, dtype=torch.bfloat16, device=f"cuda:{tdev}")
+    vo = torch.empty_like(ko)
+    idx = torch.empty(Ll, Hl, K, dtype=torch.int32, device=f"cuda:{tdev}")
+    y = torch.empty(Ll, Hl, N, device=f"cuda:{tdev}")
+    ps = torch.cuda.Stream(device=0)
+    ts = torch.cuda.Stream(device=tdev)
+    pr.run_two_device(tctx, q, kp, kt, vt, ko, vo, idx, y, proxy_stream=ps, target_stream=ts)
+    torch.cuda.synchronize(0)
+    torch.cuda.synchronize(tdev)
+    ko1 = torch.empty(Ll, Hl, K, dt, dtype=torch.bfloat16, device="cuda:0")
+    vo1 = torch.empty_like(ko1)
+    idx1 = torch.empty(Ll, Hl, K, dtype=torch.int32, device="cuda:0")
+    y1 = torch.empty(Ll, Hl, N, device="cuda:0")
+    pr.run(q, kp, dev(tiny["kt"]), dev(tiny["vt"]), ko1, vo1, idx1, y1)
+    torch.cuda.synchronize(0)
+    assert torch.equal(idx.cpu(), idx1.cpu()) and torch.equal(y.cpu(), y1.cpu())
+    assert torch.equal(_t(ko.cpu()), _t(ko1.cpu())) and torch.equal(_t(vo.cpu()), _t(vo1.cpu()))
