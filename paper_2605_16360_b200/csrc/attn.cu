@@ -322,13 +322,12 @@ void launch_encoder_attention(const __half* qkv, int64_t nwin, int64_t Lw, int64
     // kernel table: [mode 0 with kPolyPairs 2 | 4 | 6 of 16, timing probe]
     using KernT = decltype(&attn_kernel<0, 4>);
     static KernT table[4] = {attn_kernel<0, 2>, attn_kernel<0, 4>, attn_kernel<0, 6>, attn_kernel<1, 0>};
-    static bool attr = false;
+    static std::atomic<uint64_t> attr{0};
     static int pick = 1;
-    if (!attr) {
+    if (first_on_device(attr)) {
         for (KernT k : table) PKV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
         if (const char* e = getenv("PKV_ATTN_POLY")) pick = atoi(e) <= 2 ? 0 : (atoi(e) <= 4 ? 1 : 2);
         if (const char* e = getenv("PKV_ATTN_MODE")) pick = atoi(e) == 1 ? 3 : pick;  // timing probe, no exponentials
-        attr = true;
     }
     const CUtensorMap tq = make_tmap_3d(qkv, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, (uint64_t)(3 * D), (uint64_t)Lw,
                                         (uint64_t)nwin, (uint64_t)(3 * D) * 2, (uint64_t)(3 * D) * 2 * Lw, kD, kBQ, 1,

@@ -534,11 +534,8 @@ template <int BN, int NA, int NB, int EPI>
 void launch(const GemmArgs& g, int sm_count, cudaStream_t st) {
     using C = Cfg<BN, NA, NB>;
     auto kern = gemm_kernel<BN, NA, NB, EPI>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        PKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-        attr_set = true;
-    }
+    static std::atomic<uint64_t> attr_set{0};
+    if (first_on_device(attr_set)) PKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     const int64_t tiles = ((g.M + kBM - 1) / kBM) * ((g.N + BN - 1) / BN);
     const int grid = (int)(tiles < sm_count ? tiles : sm_count);
     kern<<<grid, kThreads, C::kSmem, st>>>(g.a[0], g.a[1], g.b[0], g.b[1], g.p, g.M, g.N, g.K);
@@ -781,11 +778,8 @@ template <int NA, int NB, int EPI>
 void launch2(const GemmArgs& g, int sm_count, cudaStream_t st) {
     using C = Cfg2<NA, NB, EPI>;
     auto kern = gemm2_kernel<NA, NB, EPI>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        PKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-        attr_set = true;
-    }
+    static std::atomic<uint64_t> attr_set{0};
+    if (first_on_device(attr_set)) PKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     // B re-encoded with 128-row boxes (each CTA of the pair loads half of the N tile)
     CUtensorMap b[2];
     for (int q = 0; q < NB; ++q) {

@@ -84,6 +84,16 @@ struct pkv_ctx_s {
 namespace pkv {
 
 void require_ctx(pkv_ctx ctx);
+
+// One-time setup per (call site, device): kernel attributes such as the
+// dynamic shared-memory limit are per device, so a process driving several
+// GPUs (the two-device mode, one host thread per GPU) must set them on each.
+inline bool first_on_device(std::atomic<uint64_t>& done) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    return (done.fetch_or(bit) & bit) == 0;
+}
 inline void count_launch(pkv_ctx ctx, int n = 1) { ctx->launches += n; }
 void check_launch(const char* what);
 

@@ -316,11 +316,9 @@ template <int D>
 void run_prefill(const ScoreShape& s, const void* q, const void* k, const void* v, void* o, float* lse,
                  cudaStream_t st) {
     using C = PF<D>;
-    static bool once = false;
-    if (!once) {
+    static std::atomic<uint64_t> once{0};
+    if (first_on_device(once))
         PKV_CUDA(cudaFuncSetAttribute(prefill_attn_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-        once = true;
-    }
     const CUtensorMap tq = make_tmap_3d(q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, s.Nq, s.L * s.Hq, D * 2, D * 2 * s.Nq,
                                         64, C::kBQ, 1, CU_TENSOR_MAP_SWIZZLE_128B);
     const CUtensorMap tk = make_tmap_3d(k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, s.Nk, s.L * s.Hkv, D * 2, D * 2 * s.Nk,

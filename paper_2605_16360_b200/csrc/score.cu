@@ -510,15 +510,14 @@ void set_smem(K kern, int bytes) {
 template <int D>
 void run_lse(const ScoreShape& s, const void* q, const void* k, float* lse, __nv_bfloat16* lam, cudaStream_t st) {
     using C = P1<D>;
-    static bool once = false;
+    static std::atomic<uint64_t> once{0};
     static int poly = 10;
     using KernT = decltype(&score_lse_kernel<D, 12>);
     static KernT table[5] = {score_lse_kernel<D, 6>, score_lse_kernel<D, 8>, score_lse_kernel<D, 10>,
                              score_lse_kernel<D, 12>, score_lse_kernel<D, 14>};
-    if (!once) {
+    if (first_on_device(once)) {
         for (KernT k : table) set_smem(k, C::kSmem);
         if (const char* e = getenv("PKV_POLY_PAIRS")) poly = atoi(e);  // tuning knob: 6..14 of 32 pairs
-        once = true;
     }
     const CUtensorMap tq = make_tmap_3d(q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, s.Nq, s.L * s.Hq, D * 2, D * 2 * s.Nq,
                                         64, C::kBQ, 1, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -536,11 +535,10 @@ template <int D>
 void run_pool(const ScoreShape& s, const void* q, const void* k, const __nv_bfloat16* lam, bool reduce_max, float* x,
               cudaStream_t st) {
     using C = P2<D>;
-    static bool once = false;
-    if (!once) {
+    static std::atomic<uint64_t> once{0};
+    if (first_on_device(once)) {
         set_smem(score_pool_kernel<D, true>, C::kSmem);
         set_smem(score_pool_kernel<D, false>, C::kSmem);
-        once = true;
     }
     const CUtensorMap tq = make_tmap_3d(q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, s.Nq, s.L * s.Hq, D * 2, D * 2 * s.Nq,
                                         64, C::kBQ, 1, CU_TENSOR_MAP_SWIZZLE_128B);
