@@ -256,10 +256,12 @@ void launch_conv1_im2col(const MapperSrc& s, const float* inv_mean, const float*
     WinSrc w{s.x, s.unit_off, s.win_off, s.head_stride, s.W, s.Lw, s.hs};
     const size_t smem = sizeof(float) * ((size_t)mid * (s.hs * 3 + 1) + (size_t)s.hs * (kConvTok + 4) +
                                          (size_t)(kConvTok + 2) * mid);
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
+    static std::atomic<size_t> attr[64];  // per device (the limit is a per-device function attribute)
+    int dev = 0;
+    PKV_CUDA(cudaGetDevice(&dev));
+    if (smem > 48 * 1024 && smem > attr[dev & 63].load()) {
         PKV_CUDA(cudaFuncSetAttribute(conv1_im2col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = smem;
+        attr[dev & 63] = smem;
     }
     const dim3 grid((unsigned)((s.Lw + kConvTok - 1) / kConvTok), (unsigned)(s.units * s.W));
     conv1_im2col_kernel<<<grid, 256, smem, st>>>(w, inv_mean, w1, b1, mid, col_h, col_l);
