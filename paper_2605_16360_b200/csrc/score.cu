@@ -20,6 +20,8 @@
 // q bf16 [L, Hq, Nq, d], k bf16 [L, Hkv, Nk, d]; d ∈ {64, 128}.
 #include <cstdlib>
 
+#include <mutex>
+
 #include "score.cuh"
 #include "sm100.cuh"
 
@@ -147,13 +149,92 @@ __device__ __forceinline__ void lse_chunk(const uint32_t (&ra)[32], const uint32
     m = mn;
 }
 
+// The same over a fixed per-row reference m (an upper bound of every score of
+// the row, so no running max, no max tree and no rescale): all exponents are
+// <= 0 and the sum keeps full relative precision as long as the row's largest
+// term is not far below 1 (checked by the caller).
+template <int kPolyPairs>
+__device__ __forceinline__ float lse_chunk_fixed(const uint32_t (&ra)[32], const uint32_t (&rb)[32], int valid,
+                                                 uint64_t cc, uint64_t nm, uint64_t mp) {
+    const bool masked = __any_sync(0xffffffffu, valid < 64);
+    uint64_t acc0 = pack2(0.0f, 0.0f), acc1 = acc0;
+    if (!masked) {
+#pragma unroll
+        for (int pr = 0; pr < 32; ++pr) {
+            const uint64_t s2 = pr < 16 ? pack2(__uint_as_float(ra[2 * pr]), __uint_as_float(ra[2 * pr + 1]))
+                                        : pack2(__uint_as_float(rb[2 * pr - 32]), __uint_as_float(rb[2 * pr - 31]));
+            uint64_t e;
+            if (((pr + 1) * kPolyPairs) / 32 != (pr * kPolyPairs) / 32) {
+                e = ex2_poly2_fused(s2, cc, mp);
+            } else {
+                const float2 x = unpack2(ffma2(s2, cc, nm));
+                e = pack2(ex2(x.x), ex2(x.y));
+            }
+            if (pr & 1) acc1 = fadd2(acc1, e);
+            else acc0 = fadd2(acc0, e);
+        }
+    } else {
+#pragma unroll
+        for (int pr = 0; pr < 32; ++pr) {
+            float a = pr < 16 ? __uint_as_float(ra[2 * pr]) : __uint_as_float(rb[2 * pr - 32]);
+            float b = pr < 16 ? __uint_as_float(ra[2 * pr + 1]) : __uint_as_float(rb[2 * pr - 31]);
+            a = 2 * pr < valid ? a : -INFINITY;
+            b = 2 * pr + 1 < valid ? b : -INFINITY;
+            const float2 x = unpack2(ffma2(pack2(a, b), cc, nm));
+            const uint64_t e = pack2(ex2(x.x), ex2(x.y));
+            if (pr & 1) acc1 = fadd2(acc1, e);
+            else acc0 = fadd2(acc0, e);
+        }
+    }
+    const float2 ssum = unpack2(fadd2(acc0, acc1));
+    return ssum.x + ssum.y;
+}
+
+// max_k |k| per (layer, KV head) slab: the Cauchy–Schwarz score bound's K side
+__global__ void kmax_norm_kernel(const __nv_bfloat16* __restrict__ k, int64_t rows, int d, float* __restrict__ out) {
+    const int64_t slab = blockIdx.x;
+    const __nv_bfloat16* kp = k + slab * rows * d;
+    float mx = 0.0f;
+    for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) {
+        const uint4* row = reinterpret_cast<const uint4*>(kp + r * d);
+        float s = 0.0f;
+        for (int c = 0; c < d / 8; ++c) {
+            const uint4 u = __ldg(row + c);
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float a = __uint_as_float(w[i] << 16), b = __uint_as_float(w[i] & 0xFFFF0000u);
+                s = fmaf(a, a, fmaf(b, b, s));
+            }
+        }
+        mx = fmaxf(mx, s);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __shared__ float red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = 0.0f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
+        out[slab] = sqrtf(m);
+    }
+}
+
 // ---------------------------------------------------------------- pass 1 --
-template <int D, int kPolyPairs>
+// kFixed: rows use the fixed Cauchy–Schwarz reference ceil(c·|q|·max|k|) + 1
+// (kmax) and flag their query tile when its largest term falls below 2^-40
+// (tile_flags; the exact kernel then redoes those tiles). !kFixed with
+// tile_flags: exact running-max kernel restricted to the flagged tiles.
+template <int D, int kPolyPairs, bool kFixed>
 __global__ void __launch_bounds__(P1<D>::kThreads, 1)
     score_lse_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk, int Hq, int Hkv,
                      int Nq, int Nk, int causal, float c_log2, float* __restrict__ lse_out,
-                     __nv_bfloat16* __restrict__ lam_out) {
+                     __nv_bfloat16* __restrict__ lam_out, const float* __restrict__ kmax,
+                     uint32_t* __restrict__ tile_flags) {
     using C = P1<D>;
+    const int64_t tile_id = ((int64_t)blockIdx.z * Hq + blockIdx.y) * gridDim.x + blockIdx.x;
+    if (!kFixed && tile_flags != nullptr && tile_flags[tile_id] == 0) return;  // CTA-uniform, before any barrier
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;
@@ -239,13 +320,34 @@ __global__ void __launch_bounds__(P1<D>::kThreads, 1)
         const int seg = (warp - 2) >> 2;  // column segment of the 256-key tile (quad = warp % 4)
         const int r = quad * 32 + lane;
         const int q = q0 + r;
-        const int kmax = causal ? (q + off + 1 < Nk ? q + off + 1 : Nk) : Nk;  // keys [0, kmax) allowed
+        const int kmax_k = causal ? (q + off + 1 < Nk ? q + off + 1 : Nk) : Nk;  // keys [0, kmax_k) allowed
         float m = -INFINITY, lsum = 0.0f;  // m in the log2 (scaled) domain
         constexpr int kChunks = C::kSegCols / 64;
+        uint64_t fcc = 0, fnm = 0, fmp = 0;
         for (int j = 0; j < n_kv; ++j) {
             const int sb = j & 1;
             mbar_wait(&s_full[sb], (j >> 1) & 1);
             tc_fence_after();
+            if (kFixed && j == 0) {  // Q has landed (S_0 is done): |q| of this row from the swizzled tile
+                float qn2 = 0.0f;
+#pragma unroll
+                for (int p = 0; p < C::kPanels; ++p)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const uint4 u = *reinterpret_cast<const uint4*>(sQ + p * (C::kBQ * 128) + r * 128 +
+                                                                        ((c ^ (r & 7)) * 16));
+                        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const float a = __uint_as_float(w[i] << 16), b = __uint_as_float(w[i] & 0xFFFF0000u);
+                            qn2 = fmaf(a, a, fmaf(b, b, qn2));
+                        }
+                    }
+                m = ceilf(c_log2 * sqrtf(qn2) * __ldg(kmax + kslab)) + 1.0f;
+                fcc = pack2(c_log2, c_log2);
+                fnm = pack2(-m, -m);
+                fmp = pack2(12582912.0f - m, 12582912.0f - m);
+            }
             const uint32_t base = tmem + ((quad * 32) << 16) + sb * C::kBK + seg * C::kSegCols;
             uint32_t ra[32], rb[32];
             tmem_ld32(base, ra);
@@ -262,7 +364,12 @@ __global__ void __launch_bounds__(P1<D>::kThreads, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&s_empty[sb]);
                 }
-                lse_chunk<kPolyPairs>(ra, rb, kmax - (j * C::kBK + seg * C::kSegCols + 64 * c), c_log2, m, lsum);
+                if (kFixed)
+                    lsum += lse_chunk_fixed<kPolyPairs>(ra, rb, kmax_k - (j * C::kBK + seg * C::kSegCols + 64 * c),
+                                                        fcc, fnm, fmp);
+                else
+                    lse_chunk<kPolyPairs>(ra, rb, kmax_k - (j * C::kBK + seg * C::kSegCols + 64 * c), c_log2, m,
+                                          lsum);
                 if (c + 1 < kChunks) {
                     tmem_ld_wait();
 #pragma unroll
@@ -286,6 +393,8 @@ __global__ void __launch_bounds__(P1<D>::kThreads, 1)
                 const float2 pm = part[s * C::kBQ + r];
                 L += pm.y * ex2(pm.x - M);
             }
+            // fixed reference far above the row's scores: the exact kernel redoes the tile
+            if (kFixed && !(L >= 0x1p-40f)) tile_flags[tile_id] = 1u;
             const float lse2 = M + __log2f(L);  // log2 Σ exp2(c·s)
             const int64_t row = (int64_t)qslab * Nq + q;
             if (lse_out) lse_out[row] = lse2 / kLog2e;
@@ -508,15 +617,21 @@ void set_smem(K kern, int bytes) {
 }
 
 template <int D>
-void run_lse(const ScoreShape& s, const void* q, const void* k, float* lse, __nv_bfloat16* lam, cudaStream_t st) {
+void run_lse(const ScoreShape& s, const void* q, const void* k, float* lse, __nv_bfloat16* lam, cudaStream_t st,
+             const float* kmax = nullptr, uint32_t* tile_flags = nullptr) {
     using C = P1<D>;
     static std::atomic<uint64_t> once{0};
     static int poly = 10;
-    using KernT = decltype(&score_lse_kernel<D, 12>);
-    static KernT table[5] = {score_lse_kernel<D, 6>, score_lse_kernel<D, 8>, score_lse_kernel<D, 10>,
-                             score_lse_kernel<D, 12>, score_lse_kernel<D, 14>};
+    using KernT = decltype(&score_lse_kernel<D, 12, false>);
+    static KernT table[2][5] = {{score_lse_kernel<D, 6, false>, score_lse_kernel<D, 8, false>,
+                                 score_lse_kernel<D, 10, false>, score_lse_kernel<D, 12, false>,
+                                 score_lse_kernel<D, 14, false>},
+                                {score_lse_kernel<D, 6, true>, score_lse_kernel<D, 8, true>,
+                                 score_lse_kernel<D, 10, true>, score_lse_kernel<D, 12, true>,
+                                 score_lse_kernel<D, 14, true>}};
     if (first_on_device(once)) {
-        for (KernT k : table) set_smem(k, C::kSmem);
+        for (auto& row : table)
+            for (KernT kf : row) set_smem(kf, C::kSmem);
         if (const char* e = getenv("PKV_POLY_PAIRS")) poly = atoi(e);  // tuning knob: 6..14 of 32 pairs
     }
     const CUtensorMap tq = make_tmap_3d(q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, s.Nq, s.L * s.Hq, D * 2, D * 2 * s.Nq,
@@ -525,9 +640,14 @@ void run_lse(const ScoreShape& s, const void* q, const void* k, float* lse, __nv
                                         64, C::kBK, 1, CU_TENSOR_MAP_SWIZZLE_128B);
     const dim3 grid((unsigned)((s.Nq + C::kBQ - 1) / C::kBQ), (unsigned)s.Hq, (unsigned)s.L);
     const int pi = poly <= 6 ? 0 : poly <= 8 ? 1 : poly <= 10 ? 2 : poly <= 12 ? 3 : 4;
-    auto kern = table[pi];
-    kern<<<grid, C::kThreads, C::kSmem, st>>>(tq, tk, (int)s.Hq, (int)s.Hkv, (int)s.Nq, (int)s.Nk, s.causal ? 1 : 0,
-                                              kLog2e / sqrtf((float)D), lse, lam);
+    const float c = kLog2e / sqrtf((float)D);
+    if (kmax) {  // fixed-reference pass, then the exact kernel on the flagged tiles only
+        table[1][pi]<<<grid, C::kThreads, C::kSmem, st>>>(tq, tk, (int)s.Hq, (int)s.Hkv, (int)s.Nq, (int)s.Nk,
+                                                          s.causal ? 1 : 0, c, lse, lam, kmax, tile_flags);
+        check_launch("score_lse_kernel<fixed>");
+    }
+    table[0][pi]<<<grid, C::kThreads, C::kSmem, st>>>(tq, tk, (int)s.Hq, (int)s.Hkv, (int)s.Nq, (int)s.Nk,
+                                                      s.causal ? 1 : 0, c, lse, lam, nullptr, tile_flags);
     check_launch("score_lse_kernel");
 }
 
@@ -570,10 +690,46 @@ void score_validate(const ScoreShape& s) {
     PKV_REQUIRE(!s.causal || s.Nk >= s.Nq, PKV_ECONFIG, "causal scoring needs Nk >= Nq");
 }
 
+// Scratch for the fixed-reference pass: per (layer, KV head) max |k| and one
+// flag per query tile, kept per device.
+namespace {
+struct FixedScratch {
+    DevBuf buf;
+};
+}  // namespace
+
+bool score_fixed_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("PKV_SCORE_FIXED");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
 void launch_score_lse(const ScoreShape& s, const void* q, const void* k, float* lse, __nv_bfloat16* lam,
                       cudaStream_t st) {
-    if (s.d == 64) run_lse<64>(s, q, k, lse, lam, st);
-    else run_lse<128>(s, q, k, lse, lam, st);
+    const float* kmax = nullptr;
+    uint32_t* flags = nullptr;
+    if (score_fixed_enabled()) {
+        static std::mutex mu;
+        static FixedScratch per_dev[64];
+        int dev = 0;
+        PKV_CUDA(cudaGetDevice(&dev));
+        const int64_t slabs = s.L * s.Hkv, tiles = s.L * s.Hq * ((s.Nq + 127) / 128);
+        uint8_t* w;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            w = static_cast<uint8_t*>(per_dev[dev & 63].buf.get((size_t)(slabs * 4 + 256 + tiles * 4)));
+        }
+        float* km = reinterpret_cast<float*>(w);
+        flags = reinterpret_cast<uint32_t*>(w + ((slabs * 4 + 255) & ~int64_t(255)));
+        PKV_CUDA(cudaMemsetAsync(flags, 0, (size_t)tiles * 4, st));
+        kmax_norm_kernel<<<(unsigned)slabs, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(k), s.Nk, (int)s.d, km);
+        check_launch("kmax_norm_kernel");
+        kmax = km;
+    }
+    if (s.d == 64) run_lse<64>(s, q, k, lse, lam, st, kmax, flags);
+    else run_lse<128>(s, q, k, lse, lam, st, kmax, flags);
 }
 
 void launch_lam_from_lse(const float* lse, int64_t rows, int64_t d, __nv_bfloat16* lam, cudaStream_t st) {

@@ -91,3 +91,28 @@ def test_score_shape_errors(gpu):
     with pytest.raises(P.ConfigError):
         P.score(torch.zeros(1, 1, 128, 96, dtype=torch.bfloat16, device="cuda"),
                 torch.zeros(1, 1, 128, 96, dtype=torch.bfloat16, device="cuda"), ctx=gpu)
+
+
+def test_lse_fixed_reference_fallback_tiles(gpu):
+    """Pass 1 runs against the Cauchy–Schwarz reference ceil(c·|q|·max|k|)+1;
+    rows whose largest term falls below 2^-40 of it (large norms, little
+    alignment) flag their tile and the exact running-max kernel redoes it.
+    Half the heads here are built to trip the fallback; LSE and X must match
+    the fp64 restatement everywhere."""
+    import torch
+    import paper_2605_16360_b200 as P
+    r = np.random.RandomState(11)
+    L, hq, hkv, n, d = 1, 4, 2, 512, 64
+    q = r.standard_normal((L, hq, n, d)).astype(np.float32) * 0.35
+    k = r.standard_normal((L, hkv, n, d)).astype(np.float32)
+    # KV head 1 (query heads 2, 3): huge, nearly orthogonal norms -> the bound is ~250 above the scores
+    e1, e2 = np.zeros(d, np.float32), np.zeros(d, np.float32)
+    e1[0], e2[1] = 1.0, 1.0
+    q[:, 2:] = 60.0 * e1 + 0.05 * q[:, 2:]
+    k[:, 1] = 60.0 * e2 + 0.05 * k[:, 1]
+    qb, kb = O.f32_to_bf16_bits(q), O.f32_to_bf16_bits(k)
+    lse = P.score_lse(_to_dev(qb), _to_dev(kb), ctx=gpu).cpu().numpy()
+    ref = O.score_lse(qb, kb)
+    assert np.abs(lse - ref).max() < 2e-4
+    x = P.score(_to_dev(qb), _to_dev(kb), ctx=gpu).cpu().numpy()
+    _check(x, O.score(qb, kb, reduce="max"))
