@@ -454,6 +454,20 @@ def main():
         prof = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(prof):
             roof["traffic"] = json.load(open(prof)).get(roof["kernel"])
+        if roof["kernel"] == "score_lse" and r.get("clocks", {}).get("sm_mhz"):
+            # the pass's real bound: exponentials on the MUFU (16 ex2/clk/SM) with
+            # kPolyPairs of every 32 pairs on the FMA pipe, at the measured SM clock
+            import torch
+            poly = int(os.environ.get("PKV_POLY_PAIRS", "10"))
+            exps = c["N"] * c["N"] * c["Hq"] * c["Ls"]
+            on_mufu = exps * (32 - poly) / 32
+            sms = torch.cuda.get_device_properties(0).multi_processor_count
+            peak_exp = 16 * sms * r["clocks"]["sm_mhz"] * 1e6
+            ach_exp = on_mufu / (st["score_lse_ms"] * 1e-3)
+            roof["exp_pipe"] = {"exponentials": exps, "on_mufu": on_mufu, "achieved_mufu_ex2_per_s": ach_exp,
+                                "peak_ex2_per_s_at_measured_clock": peak_exp, "frac": ach_exp / peak_exp,
+                                "note": f"{poly} of 32 pairs use the FMA-pipe polynomial; peak = 16/clk/SM x "
+                                        f"{sms} SMs x median SM clock under load"}
         sc_b = bytes_select(c) + bytes_compact(c)
         sc_ms = st["select_ms"] + st["compact_ms"]
         line["stages_ms"] = {k[:-3]: v for k, v in st.items() if not k.startswith("x_")}
