@@ -55,7 +55,7 @@ __global__ void window_mean_kernel(WinSrc src, float* __restrict__ mean_out) {
     }
 }
 
-constexpr int kConvTok = 32;  // tokens per block
+constexpr int kConvTok = 64;  // tokens per block (amortises the per-block weight staging)
 
 // z1[c, t] = gelu(b1'[c] + Σ_ci Σ_tap W1'[c, ci, tap] · x_pad[ci, t + tap - 1]) (BN folded)
 // im2col row t = [z1[t-1] | z1[t] | z1[t+1]] with zero padding at the window edges.
@@ -98,14 +98,23 @@ __global__ void conv1_im2col_kernel(WinSrc src, const float* __restrict__ inv_me
     }
     __syncthreads();
     const int64_t K = 3 * (int64_t)mid;
-    for (int tt = 0; tt < kConvTok; ++tt) {
-        const int t = t0 + tt;
-        if (t >= src.Lw) break;
-        const int64_t row = (int64_t)uw * src.Lw + t;
-        for (int i = tid; i < 3 * mid; i += blockDim.x) {
-            const int tap = i / mid, c = i % mid;
-            store_split(col_h, col_l, row * K + i, sz[(tt + tap) * mid + c]);
+    // 16-byte stores: 8 consecutive panel columns (never straddling a tap: mid % 8 == 0)
+    const int chunks = (3 * mid) / 8;
+    const int ntok = min(kConvTok, src.Lw - t0);
+    for (int i = tid; i < ntok * chunks; i += blockDim.x) {
+        const int tt = i / chunks, col = (i % chunks) * 8;
+        const int tap = col / mid, c = col % mid;
+        const float* zr = sz + (tt + tap) * mid + c;
+        __align__(16) __half hi[8];
+        __align__(16) __half lo[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            hi[e] = __float2half_rn(zr[e]);
+            lo[e] = __float2half_rn(zr[e] - __half2float(hi[e]));
         }
+        const int64_t off = ((int64_t)uw * src.Lw + t0 + tt) * K + col;
+        *reinterpret_cast<uint4*>(col_h + off) = *reinterpret_cast<const uint4*>(hi);
+        if (col_l) *reinterpret_cast<uint4*>(col_l + off) = *reinterpret_cast<const uint4*>(lo);
     }
 }
 
