@@ -231,7 +231,7 @@ pkv_status pkv_score(pkv_ctx ctx, const void* q_dev, const void* k_dev, int64_t 
         if (lse_dev) {
             pkv::launch_lam_from_lse(lse_dev, L * Hq * Nq, d, lam, st);
         } else {
-            pkv::launch_score_lse(s, q_dev, k_dev, nullptr, lam, st);
+            pkv::launch_score_lse(s, q_dev, k_dev, nullptr, lam, st, &ctx->scratch_score_aux);
         }
         pkv::launch_score_pool(s, q_dev, k_dev, lam, (flags & PKV_SCORE_REDUCE_SUM) == 0, x_out_dev, st);
         pkv::count_launch(ctx, 2);
@@ -244,7 +244,8 @@ pkv_status pkv_score_lse(pkv_ctx ctx, const void* q_dev, const void* k_dev, int6
         pkv::require_ctx(ctx);
         pkv::ScoreShape s{L, Hq, Hkv, Nq, Nk, d, (flags & PKV_SCORE_CAUSAL) != 0};
         pkv::score_validate(s);
-        pkv::launch_score_lse(s, q_dev, k_dev, lse_out_dev, nullptr, static_cast<cudaStream_t>(stream));
+        pkv::launch_score_lse(s, q_dev, k_dev, lse_out_dev, nullptr, static_cast<cudaStream_t>(stream),
+                              &ctx->scratch_score_aux);
         pkv::count_launch(ctx);
     });
 }

@@ -79,6 +79,7 @@ struct pkv_ctx_s {
     pkv::DevBuf scratch_score;
     pkv::DevBuf scratch_decode;
     pkv::DevBuf scratch_metrics;
+    pkv::DevBuf scratch_score_aux;  // fixed-reference pass 1: max |k| + tile flags
 };
 
 namespace pkv {

@@ -26,6 +26,7 @@ struct pkv_pruner_s {
     std::vector<int64_t> unit_off;  // mapper units (unique proxy layers of target layers [a, b))
     std::vector<int> out_unit;      // target layer a + i -> unit
     DevBuf lam, x, y, y_local, idx;
+    DevBuf score_aux;  // fixed-reference pass 1 scratch
     DevBuf y_remote;  // two-device mode: Ŷ on the target device (allocated there)
     cudaEvent_t ev_remote = nullptr;
     DevBuf host_in, host_out;  // device copies for the host-buffer form
@@ -174,7 +175,7 @@ void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, con
         auto* lam = static_cast<__nv_bfloat16*>(p->lam.get(static_cast<size_t>(s.L * s.Hq * s.Nq) * 16));
         auto* x = static_cast<float*>(p->x.get(static_cast<size_t>(s.L * s.Hkv * s.Nk) * 4));
         if (!arr) {
-            launch_score_lse(s, qp, kpp, nullptr, lam, ps);
+            launch_score_lse(s, qp, kpp, nullptr, lam, ps, &p->score_aux);
             launch_score_pool(s, qp, kpp, lam, p->reduce_max, x, ps);
             count_launch(p->ctx, 2);
         } else {  // proxy layers scored chunk by chunk as their H2D copies land
@@ -187,7 +188,7 @@ void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, con
                 const auto* qc = qp + static_cast<size_t>(l0 * p->Hq * p->N * p->dp) * 2;
                 const auto* kc = kpp + static_cast<size_t>(l0 * s.Hkv * p->N * p->dp) * 2;
                 __nv_bfloat16* lc = lam + static_cast<size_t>(l0 * s.Hq * s.Nq) * 8;
-                launch_score_lse(sc, qc, kc, nullptr, lc, ps);
+                launch_score_lse(sc, qc, kc, nullptr, lc, ps, &p->score_aux);
                 launch_score_pool(sc, qc, kc, lc, p->reduce_max, x + static_cast<size_t>(l0 * s.Hkv * s.Nk), ps);
                 count_launch(p->ctx, 2);
             }
@@ -280,7 +281,7 @@ pkv_status pkv_pruner_run_two_device(pkv_pruner p, pkv_ctx target_ctx, const voi
             const ScoreShape& s = p->score;
             auto* lam = static_cast<__nv_bfloat16*>(p->lam.get(static_cast<size_t>(s.L * s.Hq * s.Nq) * 16));
             auto* x = static_cast<float*>(p->x.get(static_cast<size_t>(s.L * s.Hkv * s.Nk) * 4));
-            launch_score_lse(s, q_dev, kp_dev, nullptr, lam, ps);
+            launch_score_lse(s, q_dev, kp_dev, nullptr, lam, ps, &p->score_aux);
             launch_score_pool(s, q_dev, kp_dev, lam, p->reduce_max, x, ps);
             count_launch(p->ctx, 2);
             p->mapper->run(x, p->unit_off, p->N, p->out_unit, y_p, ps);

@@ -690,14 +690,6 @@ void score_validate(const ScoreShape& s) {
     PKV_REQUIRE(!s.causal || s.Nk >= s.Nq, PKV_ECONFIG, "causal scoring needs Nk >= Nq");
 }
 
-// Scratch for the fixed-reference pass: per (layer, KV head) max |k| and one
-// flag per query tile, kept per device.
-namespace {
-struct FixedScratch {
-    DevBuf buf;
-};
-}  // namespace
-
 bool score_fixed_enabled() {
     static const bool on = [] {
         const char* e = getenv("PKV_SCORE_FIXED");
@@ -707,22 +699,15 @@ bool score_fixed_enabled() {
 }
 
 void launch_score_lse(const ScoreShape& s, const void* q, const void* k, float* lse, __nv_bfloat16* lam,
-                      cudaStream_t st) {
+                      cudaStream_t st, DevBuf* aux) {
     const float* kmax = nullptr;
     uint32_t* flags = nullptr;
-    if (score_fixed_enabled()) {
-        static std::mutex mu;
-        static FixedScratch per_dev[64];
-        int dev = 0;
-        PKV_CUDA(cudaGetDevice(&dev));
+    if (aux && score_fixed_enabled()) {
         const int64_t slabs = s.L * s.Hkv, tiles = s.L * s.Hq * ((s.Nq + 127) / 128);
-        uint8_t* w;
-        {
-            std::lock_guard<std::mutex> lk(mu);
-            w = static_cast<uint8_t*>(per_dev[dev & 63].buf.get((size_t)(slabs * 4 + 256 + tiles * 4)));
-        }
+        const int64_t kbytes = (slabs * 4 + 255) & ~int64_t(255);
+        auto* w = static_cast<uint8_t*>(aux->get((size_t)(kbytes + tiles * 4)));
         float* km = reinterpret_cast<float*>(w);
-        flags = reinterpret_cast<uint32_t*>(w + ((slabs * 4 + 255) & ~int64_t(255)));
+        flags = reinterpret_cast<uint32_t*>(w + kbytes);
         PKV_CUDA(cudaMemsetAsync(flags, 0, (size_t)tiles * 4, st));
         kmax_norm_kernel<<<(unsigned)slabs, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(k), s.Nk, (int)s.d, km);
         check_launch("kmax_norm_kernel");
