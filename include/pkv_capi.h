@@ -211,6 +211,8 @@ pkv_status pkv_mapper_init_params(const int64_t* geom5, const int64_t* cfg12, ui
 #define PKV_MAPPER_FP16X2 2u /* activations split hi+lo fp16 (2 MMAs per product) */
 #define PKV_MAPPER_FP16X3 3u /* activations and weights split (3 MMAs per product) */
 #define PKV_MAPPER_FP16W2 4u /* weights split hi+lo fp16, activations fp16 (2 MMAs per product) */
+#define PKV_MAPPER_FP16X3F 5u /* FP16X3 except the FFN down-projection, whose GELU input is one fp16
+                                 plane (2 MMAs there; its hidden activations are half the bytes) */
 
 /* Uploads a mapper (weights in the pkv_mapper_init_params layout, fp64) to the
  * device; prepares the B200 weight layouts (K-major fp16 planes, BN folded,

@@ -277,9 +277,10 @@ Mapper::Mapper(pkv_ctx c, const Geometry& g, const Config& cf, const double* blo
     : ctx(c), geom(g), cfg(cf) {
     geom.validate();
     cfg.validate();
-    PKV_REQUIRE(precision >= 1 && precision <= 4, PKV_ECONFIG, "unknown mapper precision mode ", precision);
-    na = (precision == 2 || precision == 3) ? 2 : 1;
-    nb = (precision == 3 || precision == 4) ? 2 : 1;
+    PKV_REQUIRE(precision >= 1 && precision <= 5, PKV_ECONFIG, "unknown mapper precision mode ", precision);
+    na = (precision == 2 || precision == 3 || precision == 5) ? 2 : 1;
+    nb = (precision == 3 || precision == 4 || precision == 5) ? 2 : 1;
+    ffn2_single_act = precision == 5;
     const int64_t D = cfg.d_time;
     PKV_REQUIRE(D % 128 == 0 && D <= 1024, PKV_ECONFIG, "GPU mapper needs d_time % 128 == 0 and <= 1024, got ", D);
     if (cfg.enc_active && cfg.encoder_layers > 0) {
@@ -442,7 +443,7 @@ int pick_bn(int64_t n) { return n <= 64 ? 64 : (n <= 128 ? 128 : 256); }
 }  // namespace
 
 void Mapper::gemm(const __half* a_h, const __half* a_l, int64_t M, const WeightPlanes& w, const float* bias,
-                  GemmEpi epi, GemmEpiParams p, cudaStream_t st, bool single) {
+                  GemmEpi epi, GemmEpiParams p, cudaStream_t st, bool single, bool a_single) {
     GemmArgs g;
     g.bn = pick_bn(w.N);
     g.pair = use_pair && w.N >= 256 && M >= 256;  // cta_group::2 256x256 tiles for the big projections
@@ -450,7 +451,7 @@ void Mapper::gemm(const __half* a_h, const __half* a_l, int64_t M, const WeightP
     gemm_set_a(g, 0, a_h, M, w.K, w.K);
     g.a[1] = g.a[0];
     g.na = 1;
-    if (na > 1 && !single) gemm_set_a(g, 1, a_l, M, w.K, w.K);
+    if (na > 1 && !single && !a_single) gemm_set_a(g, 1, a_l, M, w.K, w.K);
     gemm_set_b(g, 0, w.hi, w.N, w.K, w.K);
     g.b[1] = g.b[0];
     g.nb = 1;
@@ -568,13 +569,13 @@ void Mapper::run(const float* x, const std::vector<int64_t>& unit_off, int64_t N
                 count_launch(ctx);
                 GemmEpiParams pf;
                 pf.out_h = f_h;
-                pf.out_l = f_l;
+                pf.out_l = ffn2_single_act ? nullptr : f_l;  // mode 5: FFN2 reads one activation plane
                 pf.ldo = F;
                 gemm(h_h, h_l, rows, b.f1, b.f1_b, EPI_GELU_F16X, pf, st);
                 GemmEpiParams p2;
                 p2.out_f32 = z;
                 p2.ldo = D;
-                gemm(f_h, f_l, rows, b.f2, b.f2_b, EPI_RESID, p2, st);
+                gemm(f_h, f_l, rows, b.f2, b.f2_b, EPI_RESID, p2, st, false, ffn2_single_act);
             }
         } else {
             launch_window_colmean_add(z, nu * W, static_cast<int>(Lw), static_cast<int>(D), st);

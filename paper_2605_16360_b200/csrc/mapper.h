@@ -59,6 +59,7 @@ public:
     Geometry geom;
     Config cfg;
     int na = 2, nb = 1;
+    bool ffn2_single_act = false;  // precision mode 5
     int64_t rows_cap = int64_t(1) << 20;  // rows per chunk (bounds the workspace)
     bool use_pair = getenv("PKV_NO_PAIR") == nullptr;  // CTA-pair GEMMs (tuning/AB switch)
     // QKV projection with one fp16 MMA (its output is rounded to one fp16 plane
@@ -69,7 +70,7 @@ public:
 private:
     WeightPlanes upload_planes(const std::vector<double>& W, int64_t N, int64_t K);
     void gemm(const __half* a_h, const __half* a_l, int64_t M, const WeightPlanes& w, const float* bias, GemmEpi epi,
-              GemmEpiParams p, cudaStream_t st, bool single = false);
+              GemmEpiParams p, cudaStream_t st, bool single = false, bool a_single = false);
 
     std::vector<void*> owned;
     DevBuf work;

@@ -39,6 +39,8 @@ SCORE_CAUSAL = 2
 MAPPER_FP16 = 1
 MAPPER_FP16X2 = 2
 MAPPER_FP16X3 = 3
+MAPPER_FP16W2 = 4
+MAPPER_FP16X3F = 5
 SHARD_LAYER = 0
 SHARD_HEAD = 1
 COMM_ID_BYTES = 128
