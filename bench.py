@@ -272,6 +272,11 @@ def stage_breakdown(P, ctx, mapper, c, q, kp, kt, vt, ko, vo, K, stream, args):
         lambda: P.proxy_prefill_attention(q, kp, vp, causal=True, want_out=True, ctx=ctx, stream=stream), it, stream)
     out["x_score_pool_causal_ms"] = time_loop(
         lambda: P.score(q, kp, lse=plse, causal=True, ctx=ctx, stream=stream, out=x), it, stream)
+    # the whole prune in that regime: causal pruner fed the prefill LSE (pkv_pruner_run_lse)
+    prc = P.Pruner(mapper, c["Hq"], c["dp"], c["dt"], c["N"], c["rho"], causal=True)
+    prc.run_lse(q, kp, plse, kt, vt, ko, vo, stream=stream)
+    out["x_prune_with_prefill_lse_ms"] = time_loop(lambda: prc.run_lse(q, kp, plse, kt, vt, ko, vo, stream=stream),
+                                                   it, stream)
     return out
 
 
@@ -477,7 +482,9 @@ def main():
                     "SURVEY 8(f)-1): one tensor-core pass; the prefill attention itself is proxy-model work",
             "proxy_prefill_attn_ms": st["x_prefill_attn_causal_ms"], "score_pool_ms": st["x_score_pool_causal_ms"],
             "TFLOP/s": fc / st["x_score_pool_causal_ms"] / 1e9,
-            "frac_of_burst": fc / st["x_score_pool_causal_ms"] / 1e9 / tf_burst}
+            "frac_of_burst": fc / st["x_score_pool_causal_ms"] / 1e9 / tf_burst,
+            "prune_latency_ms": st["x_prune_with_prefill_lse_ms"],
+            "prune_note": "pkv_pruner_run_lse: causal pooled pass + map + select + compact, the prefill LSE given"}
         line["stage_roofline"] = {
             "score_lse": {"TFLOP/s": flops_score_pass(c) / st["score_lse_ms"] / 1e9},
             "score_pool": {"TFLOP/s": flops_score_pass(c) / st["score_pool_ms"] / 1e9},

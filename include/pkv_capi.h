@@ -249,12 +249,21 @@ int64_t pkv_pruner_k(pkv_pruner p);
 pkv_status pkv_pruner_run(pkv_pruner p, const void* q_dev, const void* kp_dev, const void* kt_dev,
                           const void* vt_dev, void* k_out_dev, void* v_out_dev, int32_t* idx_out_dev,
                           float* scores_out_dev, void* stream);
+/* The paper regime: the row LSE comes from
+ * the proxy's own prefill attention (pkv_proxy_prefill_attention, natural
+ * log, fp32 [L_s, Hq, N], with the pruner's causal flag), so scoring is the
+ * pooled pass alone. Otherwise as pkv_pruner_run. */
+pkv_status pkv_pruner_run_lse(pkv_pruner p, const void* q_dev, const void* kp_dev, const float* lse_dev,
+                              const void* kt_dev, const void* vt_dev, void* k_out_dev, void* v_out_dev,
+                              int32_t* idx_out_dev, float* scores_out_dev, void* stream);
 /* Same with host buffers: H2D of the inputs and D2H of the outputs are part
  * of the call (the reference-facing end-to-end form). The copies run on the
- * pruner's own stream, overlapped with compute: the proxy Q/K in four
- * layer chunks (each chunk's scoring starts when it lands), then the target
- * KV (consumed only by select + compaction, after the mapper). Pinned host
- * memory makes the copies asynchronous. */
+ * pruner's own copy stream, overlapped with compute: the proxy Q/K one proxy
+ * layer at a time (each layer's scoring starts when it lands), then the
+ * target KV (consumed only by select + compaction); the map -> select ->
+ * compact tail runs per group of target layers, each group's outputs copied
+ * back while the next group is mapped. Pinned host memory makes the copies
+ * asynchronous. */
 pkv_status pkv_pruner_run_host(pkv_pruner p, const void* q_host, const void* kp_host, const void* kt_host,
                                const void* vt_host, void* k_out_host, void* v_out_host, int32_t* idx_out_host,
                                void* stream);

@@ -87,6 +87,7 @@ SIGNATURES = {
     "pkv_paged_decode_attention": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64,
                                                   _c_i64, _c_i64, _c_i64, _c_i64, ctypes.c_double, _c_vp, _c_vp]),
     "pkv_pruner_run_two_device": (ctypes.c_int, [_c_vp] * 12),
+    "pkv_pruner_run_lse": (ctypes.c_int, [_c_vp] * 11),
     "pkv_spearman": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_vp, _c_vp]),
     "pkv_loss_total": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp, ctypes.c_int, _c_vp, ctypes.c_uint64, _c_vp, _c_vp,
                                       _c_vp]),

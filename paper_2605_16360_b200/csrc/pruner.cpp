@@ -156,7 +156,7 @@ pkv_pruner make_pruner(pkv_ctx ctx, pkv_mapper m, int64_t Hq, int64_t dp, int64_
 // event when the streams differ).
 void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, const void* vt, void* k_out,
                 void* v_out, int32_t* idx_out, float* scores_out, cudaStream_t ps, cudaStream_t ts,
-                const HostArrival* arr = nullptr) {
+                const HostArrival* arr = nullptr, const float* lse_in = nullptr) {
     const ScoreShape& s = p->score;
     const ShardPlan& pl = p->plan;
     const int64_t slices = p->slices();
@@ -174,7 +174,12 @@ void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, con
         const auto* kpp = static_cast<const uint8_t*>(kp) + k_off;
         auto* lam = static_cast<__nv_bfloat16*>(p->lam.get(static_cast<size_t>(s.L * s.Hq * s.Nq) * 16));
         auto* x = static_cast<float*>(p->x.get(static_cast<size_t>(s.L * s.Hkv * s.Nk) * 4));
-        if (!arr) {
+        if (lse_in) {  // LSE from the proxy's prefill attention: the pooled pass only
+            launch_lam_from_lse(lse_in + static_cast<size_t>(pl.p_lo * p->Hq * p->N), s.L * s.Hq * s.Nq, s.d, lam,
+                                ps);
+            launch_score_pool(s, qp, kpp, lam, p->reduce_max, x, ps);
+            count_launch(p->ctx, 2);
+        } else if (!arr) {
             launch_score_lse(s, qp, kpp, nullptr, lam, ps, &p->score_aux);
             launch_score_pool(s, qp, kpp, lam, p->reduce_max, x, ps);
             count_launch(p->ctx, 2);
@@ -244,6 +249,17 @@ pkv_status pkv_pruner_run(pkv_pruner p, const void* q, const void* kp, const voi
         PKV_REQUIRE_VALUE(p != nullptr, "null pkv_pruner");
         auto st = static_cast<cudaStream_t>(stream);
         run_pruner(p, q, kp, kt, vt, k_out, v_out, idx_out, scores_out, st, st);
+    });
+}
+
+pkv_status pkv_pruner_run_lse(pkv_pruner p, const void* q, const void* kp, const float* lse, const void* kt,
+                              const void* vt, void* k_out, void* v_out, int32_t* idx_out, float* scores_out,
+                              void* stream) {
+    return guard([&] {
+        PKV_REQUIRE_VALUE(p != nullptr, "null pkv_pruner");
+        PKV_REQUIRE_VALUE(lse != nullptr, "pkv_pruner_run_lse needs the proxy prefill's LSE");
+        auto st = static_cast<cudaStream_t>(stream);
+        run_pruner(p, q, kp, kt, vt, k_out, v_out, idx_out, scores_out, st, st, nullptr, lse);
     });
 }
 

@@ -660,6 +660,12 @@ class Pruner:
         check(lib().pkv_pruner_run(self.h, _ptr(q), _ptr(kp), _ptr(kt), _ptr(vt), _ptr(k_out), _ptr(v_out),
                                    _ptr(idx_out), _ptr(scores_out), _stream(stream)))
 
+    def run_lse(self, q, kp, lse, kt, vt, k_out, v_out, idx_out=None, scores_out=None, stream=None):
+        """Paper regime: the row LSE [L_s, Hq, N] from the proxy's prefill attention
+        (proxy_prefill_attention), so scoring is the pooled pass alone."""
+        check(lib().pkv_pruner_run_lse(self.h, _ptr(q), _ptr(kp), _ptr(lse.contiguous()), _ptr(kt), _ptr(vt),
+                                       _ptr(k_out), _ptr(v_out), _ptr(idx_out), _ptr(scores_out), _stream(stream)))
+
     def run_dual(self, q, kp, kt, vt, k_out, v_out, idx_out=None, scores_out=None, *, proxy_stream, target_stream):
         """Scoring + mapping on proxy_stream, select + compaction on target_stream."""
         check(lib().pkv_pruner_run_dual(self.h, _ptr(q), _ptr(kp), _ptr(kt), _ptr(vt), _ptr(k_out), _ptr(v_out),

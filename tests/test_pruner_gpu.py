@@ -184,3 +184,42 @@ def test_pruner_two_device_matches_single(tiny):
     torch.cuda.synchronize(0)
     assert torch.equal(idx.cpu(), idx1.cpu()) and torch.equal(y.cpu(), y1.cpu())
     assert torch.equal(_t(ko.cpu()), _t(ko1.cpu())) and torch.equal(_t(vo.cpu()), _t(vo1.cpu()))
+
+
+def test_pruner_with_prefill_lse_matches_two_pass(gpu):
+    """Paper regime: the causal pruner fed the proxy prefill's
+    own LSE (pkv_pruner_run_lse: the pooled pass only) maps to the same scores
+    as the causal two-pass pruner (rel 1e-4) and keeps >= 99.9 % of its Top-K."""
+    import torch
+    import paper_2605_16360_b200 as P
+    Ls, Hq, Hs, dp, Ll, Hl, dt, N, rho = 2, 8, 2, 64, 4, 4, 64, 2048, 0.2
+    geom = P.ModelGeometry(Ll, Hl, Ls, Hs, dt)
+    m = P.Mapper(geom, P.MapperConfig(encoder_layers=2), seed=5, ctx=gpu)
+    pr = P.Pruner(m, Hq, dp, dt, N, rho, causal=True)
+    K = pr.k
+    g = torch.Generator(device="cuda").manual_seed(9)
+    q = (torch.randn(Ls, Hq, N, dp, device="cuda", generator=g) * 0.35).to(torch.bfloat16)
+    kp = torch.randn(Ls, Hs, N, dp, device="cuda", generator=g).to(torch.bfloat16)
+    vp = torch.randn(Ls, Hs, N, dp, device="cuda", generator=g).to(torch.bfloat16)
+    kt = torch.randn(Ll, Hl, N, dt, device="cuda", generator=g).to(torch.bfloat16)
+    vt = torch.randn_like(kt)
+    _, lse = P.proxy_prefill_attention(q, kp, vp, causal=True, want_out=False, ctx=gpu)
+    outs = []
+    for use_lse in (False, True):
+        ko = torch.empty(Ll, Hl, K, dt, dtype=torch.bfloat16, device="cuda")
+        vo = torch.empty_like(ko)
+        idx = torch.empty(Ll, Hl, K, dtype=torch.int32, device="cuda")
+        y = torch.empty(Ll, Hl, N, device="cuda")
+        if use_lse:
+            pr.run_lse(q, kp, lse, kt, vt, ko, vo, idx, y)
+        else:
+            pr.run(q, kp, kt, vt, ko, vo, idx, y)
+        outs.append((idx, y))
+    torch.cuda.synchronize()
+    (i2, y2), (i1, y1) = outs
+    rel = ((y1 - y2).norm(dim=-1) / y2.norm(dim=-1)).max().item()
+    assert rel <= 1e-4, rel
+    a = i1.view(-1, K).cpu().numpy()
+    b = i2.view(-1, K).cpu().numpy()
+    ov = np.mean([len(np.intersect1d(a[s], b[s])) / K for s in range(a.shape[0])])
+    assert ov >= 0.999, ov
