@@ -224,6 +224,233 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
     }
 }
 
+// Tensor-core variant: per warp, 16-key tiles staged by cp.async into a
+// private 3-stage shared-memory ring (16-byte chunks XOR-swizzled by row, so
+// ldmatrix is conflict-free); S = Q·Kᵀ and O += P·V as mma.sync m16n8k16 with
+// the G <= 8 heads of the group as the M rows (rows G..15 are zero padding:
+// with M >= 64, tcgen05 would waste 8x more). Scores are scaled in fp32; P is
+// split into bf16 hi + lo (two MMAs) so the product keeps fp32-level accuracy
+// against the exact bf16 V. Lazy max per head (raised only by > 2^8).
+constexpr int kMmaWarps = 4;
+constexpr int kMmaStages = 3;
+constexpr int kTileKeys = 16;
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+    // A rows 8..15 (a1, a3) are zero padding
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int D>
+struct MmaCfg {
+    static constexpr int kRowBytes = D * 2;
+    static constexpr int kChunks = D / 8;  // 16-byte chunks per row
+    static constexpr int kTileBytes = kTileKeys * kRowBytes;
+    static constexpr int kStageBytes = 2 * kTileBytes;  // K | V
+    static constexpr int kSmem = kMmaWarps * kMmaStages * kStageBytes;
+};
+
+template <int D, int G>
+__global__ void __launch_bounds__(32 * kMmaWarps)
+    decode_mma_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kc,
+                      const __nv_bfloat16* __restrict__ vc, int Hq, int Hkv, int g, int64_t K, int64_t chunk,
+                      float scale_log2, float* __restrict__ part, Paged pg, bool paged) {
+    using C = MmaCfg<D>;
+    static_assert(G <= 8, "heads are the MMA rows 0..7");
+    extern __shared__ __align__(128) uint8_t dsm[];
+    const int split = blockIdx.x, kh = blockIdx.y, l = blockIdx.z;
+    const int splits = gridDim.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t kslab = (int64_t)l * Hkv + kh;
+    const int64_t len = paged ? (int64_t)__ldg(pg.lens + kslab) : K;
+    const int64_t k_lo = split * chunk, k_hi = min(len, k_lo + chunk);
+    const int64_t n_tiles = k_hi > k_lo ? (k_hi - k_lo + kTileKeys - 1) / kTileKeys : 0;
+    const int32_t* ptab = paged ? pg.table + kslab * pg.max_blocks : nullptr;
+    uint8_t* ring = dsm + warp * kMmaStages * C::kStageBytes;
+    const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
+
+    // this warp's tiles: t = warp, warp + kMmaWarps, ...
+    auto issue = [&](int64_t t, int stage) {
+        const int64_t key0 = k_lo + t * kTileKeys;
+        const uint32_t dk = ring_s + stage * C::kStageBytes, dv = dk + C::kTileBytes;
+#pragma unroll
+        for (int j = 0; j < kTileKeys * C::kChunks / 32; ++j) {
+            const int i = lane + 32 * j;
+            const int row = i / C::kChunks, c = i % C::kChunks;
+            int64_t key = key0 + row;
+            key = key < k_hi ? key : k_lo;
+            const int64_t grow = paged ? (int64_t)__ldg(ptab + key / pg.page) * pg.page + key % pg.page
+                                       : kslab * K + key;
+            const uint32_t off = row * C::kRowBytes + ((c ^ (row & 7)) << 4);
+            cp_async16(dk + off, kc + grow * D + c * 8);
+            cp_async16(dv + off, vc + grow * D + c * 8);
+        }
+    };
+
+    // Q as the A operand (head rows; rows >= g are zero): 16 dims per k-step
+    const int hrow = lane >> 2, qd = (lane & 3) * 2;
+    uint32_t qa[D / 16][2];
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+        if (hrow < g) {
+            const __nv_bfloat16* qp = q + ((int64_t)l * Hq + kh * g + hrow) * D + kk * 16 + qd;
+            qa[kk][0] = *reinterpret_cast<const uint32_t*>(qp);
+            qa[kk][1] = *reinterpret_cast<const uint32_t*>(qp + 8);
+        } else {
+            qa[kk][0] = qa[kk][1] = 0u;
+        }
+    }
+    float o[D / 8][4];
+#pragma unroll
+    for (int nd = 0; nd < D / 8; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.0f;
+    float m = -INFINITY, lsum = 0.0f;
+
+    const int64_t my_tiles = n_tiles > warp ? (n_tiles - warp + kMmaWarps - 1) / kMmaWarps : 0;
+#pragma unroll
+    for (int i = 0; i < kMmaStages - 1; ++i) {
+        if (i < my_tiles) issue(warp + (int64_t)i * kMmaWarps, i);
+        cp_async_commit();
+    }
+    for (int64_t i = 0; i < my_tiles; ++i) {
+        const int stage = (int)(i % kMmaStages);
+        if (i + kMmaStages - 1 < my_tiles) issue(warp + (i + kMmaStages - 1) * kMmaWarps, (int)((i + kMmaStages - 1) % kMmaStages));
+        cp_async_commit();
+        cp_async_wait<kMmaStages - 1>();
+        __syncwarp();
+        const uint32_t tk = ring_s + stage * C::kStageBytes, tv = tk + C::kTileBytes;
+        const int64_t key0 = k_lo + (warp + i * kMmaWarps) * kTileKeys;
+        // S = Q·Kᵀ for two 8-key blocks
+        float sacc[2][4];
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb) {
+            sacc[nb][0] = sacc[nb][1] = sacc[nb][2] = sacc[nb][3] = 0.0f;
+#pragma unroll
+            for (int kk = 0; kk < D / 16; kk += 2) {
+                const int mtx = lane >> 3, r = lane & 7;
+                const int key = nb * 8 + r, c = (kk + (mtx >> 1)) * 2 + (mtx & 1);
+                uint32_t b[4];
+                ldsm_x4(tk + key * C::kRowBytes + ((c ^ (key & 7)) << 4), b);
+                mma_bf16(sacc[nb], qa[kk][0], qa[kk][1], b[0], b[1]);
+                mma_bf16(sacc[nb], qa[kk + 1][0], qa[kk + 1][1], b[2], b[3]);
+            }
+        }
+        // softmax over this tile's keys for head row hrow (a quad of lanes holds all 16 keys)
+        float x[2][2];
+        float tmax = -INFINITY;
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int64_t key = key0 + nb * 8 + qd + j;
+                x[nb][j] = key < k_hi ? sacc[nb][j] * scale_log2 : -INFINITY;
+                tmax = fmaxf(tmax, x[nb][j]);
+            }
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+        if (tmax > m + kLazy) {  // raise the reference max (first tile always)
+            const float a = ex2(m - tmax);
+            lsum *= a;
+#pragma unroll
+            for (int nd = 0; nd < D / 8; ++nd) {
+                o[nd][0] *= a;
+                o[nd][1] *= a;
+            }
+            m = tmax;
+        }
+        float p[2][2];
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                p[nb][j] = ex2(x[nb][j] - m);
+                lsum += p[nb][j];
+            }
+        // P as the A operand, split into bf16 hi + lo
+        const uint32_t ah0 = pack_bf16(p[0][0], p[0][1]), ah2 = pack_bf16(p[1][0], p[1][1]);
+        const __nv_bfloat162 h0 = *reinterpret_cast<const __nv_bfloat162*>(&ah0);
+        const __nv_bfloat162 h2 = *reinterpret_cast<const __nv_bfloat162*>(&ah2);
+        const uint32_t al0 = pack_bf16(p[0][0] - __low2float(h0), p[0][1] - __high2float(h0));
+        const uint32_t al2 = pack_bf16(p[1][0] - __low2float(h2), p[1][1] - __high2float(h2));
+        // O += P·V, two 8-dim blocks per ldmatrix.x4.trans
+#pragma unroll
+        for (int nd = 0; nd < D / 8; nd += 2) {
+            const int mtx = lane >> 3, r = lane & 7;
+            const int key = (mtx & 1) * 8 + r, c = nd + (mtx >> 1);
+            uint32_t b[4];
+            ldsm_x4_t(tv + key * C::kRowBytes + ((c ^ (key & 7)) << 4), b);
+            mma_bf16(o[nd], ah0, ah2, b[0], b[1]);
+            mma_bf16(o[nd], al0, al2, b[0], b[1]);
+            mma_bf16(o[nd + 1], ah0, ah2, b[2], b[3]);
+            mma_bf16(o[nd + 1], al0, al2, b[2], b[3]);
+        }
+        __syncwarp();  // the stage is refilled by the next issue
+    }
+    cp_async_wait<0>();
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
+
+    // merge the kMmaWarps warp states per head
+    __shared__ float s_m[kMmaWarps][8], s_l[kMmaWarps][8];
+    __shared__ float s_o[8][D];
+    if ((lane & 3) == 0) {
+        s_m[warp][hrow] = m;
+        s_l[warp][hrow] = lsum;
+    }
+    for (int i = threadIdx.x; i < 8 * D; i += blockDim.x) s_o[i / D][i % D] = 0.0f;
+    __syncthreads();
+    float M = -INFINITY;
+    for (int w = 0; w < kMmaWarps; ++w) M = fmaxf(M, s_m[w][hrow]);
+    const float wgt = M == -INFINITY ? 0.0f : exp2f(m - M);
+    if (hrow < g) {
+#pragma unroll
+        for (int nd = 0; nd < D / 8; ++nd) {
+            atomicAdd(&s_o[hrow][nd * 8 + qd], o[nd][0] * wgt);
+            atomicAdd(&s_o[hrow][nd * 8 + qd + 1], o[nd][1] * wgt);
+        }
+    }
+    __syncthreads();
+    const int64_t pstride = 2 + D;
+    for (int i = threadIdx.x; i < g * D; i += blockDim.x) {
+        const int h = i / D, e = i % D;
+        float* pp = part + (((int64_t)l * Hq + kh * g + h) * splits + split) * pstride;
+        pp[2 + e] = s_o[h][e];
+        if (e == 0) {
+            float Mh = -INFINITY;
+            for (int w = 0; w < kMmaWarps; ++w) Mh = fmaxf(Mh, s_m[w][h]);
+            float Ls = 0.0f;
+            for (int w = 0; w < kMmaWarps; ++w)
+                Ls += s_m[w][h] == -INFINITY ? 0.0f : s_l[w][h] * exp2f(s_m[w][h] - Mh);
+            pp[0] = Mh;
+            pp[1] = Ls;
+        }
+    }
+}
+
 template <int D>
 __global__ void decode_merge_kernel(const float* __restrict__ part, int splits, float* __restrict__ out) {
     const int64_t head = blockIdx.x;  // l * Hq + h
@@ -257,10 +484,23 @@ void run_decode(const DecodeShape& s, const void* q, const void* kc, const void*
     splits = (s.K + chunk - 1) / chunk;
     float* part = static_cast<float*>(ws.get(static_cast<size_t>(s.L * s.Hq * splits * (2 + D)) * 4));
     const dim3 grid((unsigned)splits, (unsigned)s.Hkv, (unsigned)s.L);
-    auto kern = pg.table ? decode_split_kernel<D, G, true> : decode_split_kernel<D, G, false>;
-    kern<<<grid, 32 * kWarps, 0, st>>>(static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(kc),
-                                       static_cast<const __nv_bfloat16*>(vc), (int)s.Hq, (int)s.Hkv,
-                                       (int)(s.Hq / s.Hkv), s.K, chunk, s.scale * 1.4426950408889634f, part, pg);
+    static const bool mma_off = getenv("PKV_DECODE_MMA") && atoi(getenv("PKV_DECODE_MMA")) == 0;  // A/B knob
+    if (!mma_off) {
+        static std::atomic<uint64_t> attr{0};
+        if (first_on_device(attr))
+            PKV_CUDA(cudaFuncSetAttribute(decode_mma_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          MmaCfg<D>::kSmem));
+        decode_mma_kernel<D, G><<<grid, 32 * kMmaWarps, MmaCfg<D>::kSmem, st>>>(
+            static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(kc),
+            static_cast<const __nv_bfloat16*>(vc), (int)s.Hq, (int)s.Hkv, (int)(s.Hq / s.Hkv), s.K, chunk,
+            s.scale * 1.4426950408889634f, part, pg, pg.table != nullptr);
+    } else {
+        auto kern = pg.table ? decode_split_kernel<D, G, true> : decode_split_kernel<D, G, false>;
+        kern<<<grid, 32 * kWarps, 0, st>>>(static_cast<const __nv_bfloat16*>(q),
+                                           static_cast<const __nv_bfloat16*>(kc),
+                                           static_cast<const __nv_bfloat16*>(vc), (int)s.Hq, (int)s.Hkv,
+                                           (int)(s.Hq / s.Hkv), s.K, chunk, s.scale * 1.4426950408889634f, part, pg);
+    }
     check_launch("decode_split_kernel");
     decode_merge_kernel<D><<<(unsigned)(s.L * s.Hq), D, 0, st>>>(part, (int)splits, out);
     check_launch("decode_merge_kernel");
