@@ -4,11 +4,14 @@
 //
 //   pass 1 (score_lse_kernel):  S = Q·Kᵀ (M = 128 queries, N = 256 keys) into
 //     double-buffered TMEM; 16 softmax warps (4 column segments x 4 TMEM lane
-//     quadrants) keep an online (max, Σexp2) per row segment in registers,
-//     merged through smem at the end; ~7 in 16 exponentials are evaluated as a
-//     degree-3 polynomial on the FMA pipe to offload MUFU (FA4-style), with
-//     the integer row max folded into the range reduction; writes
-//     lse[q] and the bf16 triple (hi, mid, lo) of λ_q = √d·lse_q.
+//     quadrants) sum exp2(c·s − m) per row segment in registers against a
+//     fixed per-row reference m = ⌈c·|q|·max|k|⌉ + 1 (Cauchy–Schwarz: no
+//     running max), merged through smem at the end; 10 of 32 exponential
+//     pairs are a degree-3 polynomial on the FMA pipe to offload MUFU
+//     (FA4-style), with m folded into the range reduction; writes lse[q] and
+//     the bf16 triple (hi, mid, lo) of λ_q = √d·lse_q. A row whose largest
+//     term falls below 2^-40 flags its tile; the exact running-max variant of
+//     the kernel then redoes only the flagged tiles.
 //   pass 2 (score_pool_kernel): S' = K·Qᵀ − λ (two M = 128 key blocks = 256
 //     keys per CTA, N = 128 queries per tile), the −λ_q column folded into the
 //     MMA as 3 extra K columns (K_aug = 1, Q_aug = −(hi, mid, lo)); one thread
