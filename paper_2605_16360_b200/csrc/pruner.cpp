@@ -34,7 +34,7 @@ struct pkv_pruner_s {
     // host-buffer form: copy stream + events (proxy layer chunks, target KV)
     cudaStream_t copy_st = nullptr;
     static constexpr int kChunks = 16;  // proxy-layer chunks of the H2D
-    static constexpr int kGroups = 4;   // target-layer groups of the map -> select -> compact -> D2H tail
+    static constexpr int kGroups = 8;   // target-layer groups of the map -> select -> compact -> D2H tail
     cudaEvent_t ev_in[kChunks + 2] = {};
     cudaEvent_t ev_grp[kGroups + 1] = {};
     ~pkv_pruner_s() {
