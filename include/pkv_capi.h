@@ -75,8 +75,16 @@ pkv_status pkv_retention_count(double rho, int64_t n, int64_t* k_out);
 pkv_status pkv_topk_select(pkv_ctx ctx, const float* scores_dev, int64_t slices, int64_t n, int64_t k,
                            uint8_t* mask_dev, int32_t* idx_asc_dev, void* stream);
 
-/* Host-buffer form of topk_mask (pruning.cpp:37-56): fp64 scores (must be
- * fp32-representable for bit-exact parity) -> mask bits; H2D/D2H inside. */
+/* fp64 device scores [slices, n] (the reference's ScoreTensor element type,
+ * tensor.hpp:86): same contract as pkv_topk_select, ranked on 64-bit order keys
+ * so distinct doubles never collide (replaces topk_indices / topk_mask,
+ * pruning.cpp:20-56, on arbitrary double inputs, bit-exact). */
+pkv_status pkv_topk_select_f64(pkv_ctx ctx, const double* scores_dev, int64_t slices, int64_t n, int64_t k,
+                               uint8_t* mask_dev, int32_t* idx_asc_dev, void* stream);
+
+/* Host-buffer form of topk_mask (pruning.cpp:37-56): fp64 scores -> mask bits,
+ * k = retention_count(rho, n); the doubles are ranked as they are (64-bit
+ * keys, bit-exact for any input without NaN); H2D/D2H inside. */
 pkv_status pkv_topk_mask_host(pkv_ctx ctx, const double* scores_host, int64_t slices, int64_t n, double rho,
                               uint8_t* bits_host, int64_t* k_out);
 

@@ -156,21 +156,33 @@ pkv_status pkv_topk_select(pkv_ctx ctx, const float* scores_dev, int64_t slices,
     });
 }
 
+pkv_status pkv_topk_select_f64(pkv_ctx ctx, const double* scores_dev, int64_t slices, int64_t n, int64_t k,
+                               uint8_t* mask_dev, int32_t* idx_asc_dev, void* stream) {
+    return guard([&] {
+        require_ctx(ctx);
+        PKV_REQUIRE_SHAPE(slices >= 0 && n > 0, "topk_select needs n > 0, got n=", n);
+        PKV_REQUIRE_VALUE(k >= 1 && k <= n, "top-k count ", k, " out of range for length ", n);
+        PKV_REQUIRE_VALUE(n < (int64_t(1) << 31), "token axis too long: ", n);
+        launch_topk_select_f64(scores_dev, slices, n, k, mask_dev, idx_asc_dev, static_cast<cudaStream_t>(stream));
+        count_launch(ctx);
+    });
+}
+
 pkv_status pkv_topk_mask_host(pkv_ctx ctx, const double* scores_host, int64_t slices, int64_t n, double rho,
                               uint8_t* bits_host, int64_t* k_out) {
     return guard([&] {
         require_ctx(ctx);
         PKV_REQUIRE_SHAPE(slices > 0 && n > 0, "topk_mask needs a shaped tensor");
         PKV_REQUIRE_VALUE(rho > 0.0 && rho <= 1.0, "retention ratio must be in (0, 1], got ", rho);
+        PKV_REQUIRE_VALUE(n < (int64_t(1) << 31), "token axis too long: ", n);
         const int64_t k = static_cast<int64_t>(std::ceil(rho * static_cast<double>(n)));
         const size_t numel = static_cast<size_t>(slices * n);
-        std::vector<float> f(numel);
-        for (size_t i = 0; i < numel; ++i) f[i] = static_cast<float>(scores_host[i]);
-        auto* dev = static_cast<uint8_t*>(ctx->scratch_host_io.get(numel * 5));
-        float* d_scores = reinterpret_cast<float*>(dev);
-        uint8_t* d_mask = dev + numel * 4;
-        PKV_CUDA(cudaMemcpy(d_scores, f.data(), numel * 4, cudaMemcpyHostToDevice));
-        launch_topk_select(d_scores, slices, n, k, d_mask, nullptr, nullptr);
+        // the doubles go over as they are: 64-bit order keys rank them exactly
+        auto* dev = static_cast<uint8_t*>(ctx->scratch_host_io.get(numel * 9));
+        double* d_scores = reinterpret_cast<double*>(dev);
+        uint8_t* d_mask = dev + numel * 8;
+        PKV_CUDA(cudaMemcpy(d_scores, scores_host, numel * 8, cudaMemcpyHostToDevice));
+        launch_topk_select_f64(d_scores, slices, n, k, d_mask, nullptr, nullptr);
         count_launch(ctx);
         PKV_CUDA(cudaMemcpy(bits_host, d_mask, numel, cudaMemcpyDeviceToHost));
         *k_out = k;

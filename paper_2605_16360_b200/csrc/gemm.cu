@@ -32,75 +32,6 @@ struct Cfg {
     static_assert(kStages >= 2, "not enough shared memory for 2 stages");
 };
 
-template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(const GemmEpiParams& p, int64_t row, int64_t col0, int64_t N,
-                                               const uint32_t (&r)[32]) {
-    float v[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-    const bool full = (col0 + 32 <= N);
-    if (p.bias) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] += (full || col0 + j < N) ? __ldg(p.bias + col0 + j) : 0.0f;
-    }
-    if (EPI == EPI_GELU_F16X || EPI == EPI_GELU_PE) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
-    }
-    const int64_t base = row * p.ldo + col0;
-    if (EPI == EPI_F16X || EPI == EPI_GELU_F16X) {
-        if (full) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-                __align__(16) __half hi[8];
-                __align__(16) __half lo[8];
-#pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                    hi[t] = __float2half_rn(v[j + t]);
-                    lo[t] = __float2half_rn(v[j + t] - __half2float(hi[t]));
-                }
-                *reinterpret_cast<uint4*>(p.out_h + base + j) = *reinterpret_cast<const uint4*>(hi);
-                if (p.out_l) *reinterpret_cast<uint4*>(p.out_l + base + j) = *reinterpret_cast<const uint4*>(lo);
-            }
-        } else {
-            for (int j = 0; j < 32 && col0 + j < N; ++j) {
-                const __half hi = __float2half_rn(v[j]);
-                p.out_h[base + j] = hi;
-                if (p.out_l) p.out_l[base + j] = __float2half_rn(v[j] - __half2float(hi));
-            }
-        }
-        return;
-    }
-    if (EPI == EPI_GELU_PE && p.pe) {
-        const float* pe = p.pe + (row % p.lw) * p.ldo + col0;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] += (full || col0 + j < N) ? __ldg(pe + j) : 0.0f;
-    }
-    float* out = p.out_f32 + base;
-    if (EPI == EPI_RESID) {
-        if (full) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-                float4 o = *reinterpret_cast<float4*>(out + j);
-                o.x += v[j];
-                o.y += v[j + 1];
-                o.z += v[j + 2];
-                o.w += v[j + 3];
-                *reinterpret_cast<float4*>(out + j) = o;
-            }
-        } else {
-            for (int j = 0; j < 32 && col0 + j < N; ++j) out[j] += v[j];
-        }
-        return;
-    }
-    if (full) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(out + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-    } else {
-        for (int j = 0; j < 32 && col0 + j < N; ++j) out[j] = v[j];
-    }
-}
-
 // Warp-cooperative epilogue for a 32-row x 32-column accumulator chunk:
 // thread t holds row (row0 + t). The chunk is transposed through a padded smem
 // tile so global loads/stores are row-contiguous across the warp (128 B fp32
@@ -132,6 +63,11 @@ __device__ __forceinline__ void epilogue_row(const GemmEpiParams& p, int64_t row
     float v[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+    if ((EPI == EPI_F32 || EPI == EPI_GELU_PE) && p.row_scale) {
+        const float rs = __ldg(p.row_scale + row);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] *= rs;
+    }
     if (p.bias) {
         if (full) {
 #pragma unroll
@@ -304,9 +240,12 @@ __device__ __forceinline__ void epilogue_coalesced(const GemmEpiParams& p, int64
                 for (int rr = 0; rr < 32; ++rr) out[rr * p.ldo] = stg[rr * kStageLd + lane] + b + extra[rr];
             } else {
                 int pr = (int)(row0 % p.lw);  // window position of row0 (PE table is L2-resident)
+                const float* rsc = (EPI == EPI_F32 || EPI == EPI_GELU_PE) ? p.row_scale : nullptr;
 #pragma unroll 8
                 for (int rr = 0; rr < 32; ++rr) {
-                    float x = stg[rr * kStageLd + lane] + b;
+                    float x = stg[rr * kStageLd + lane];
+                    if (rsc) x *= __ldg(rsc + row0 + rr);
+                    x += b;
                     if (EPI == EPI_GELU_PE) {
                         x = gelu_fast(x);
                         if (p.pe) x += __ldg(p.pe + (int64_t)pr * p.ldo + col);
@@ -334,7 +273,9 @@ __device__ __forceinline__ void epilogue_coalesced(const GemmEpiParams& p, int64
 #pragma unroll
             for (int rr = 0; rr < 32; ++rr) {
                 if (!cok || row0 + rr >= M) continue;
-                float x = stg[rr * kStageLd + lane] + b;
+                float x = stg[rr * kStageLd + lane];
+                if ((EPI == EPI_F32 || EPI == EPI_GELU_PE) && p.row_scale) x *= __ldg(p.row_scale + row0 + rr);
+                x += b;
                 if (EPI == EPI_GELU_PE) {
                     x = gelu_fast(x);
                     if (p.pe) x += extra[rr];

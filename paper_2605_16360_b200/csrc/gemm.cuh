@@ -27,12 +27,20 @@ enum GemmEpi : int {
     EPI_GELU_PE = 4,     // out_f32 = gelu(acc + bias) + pe[row % lw] (conv2 + BN folded + PE)
 };
 
+// Row scaling (EPI_F32 / EPI_GELU_PE): when row_scale is set, acc is first
+// multiplied by row_scale[row]. The A-operand producers (conv1_im2col, the
+// stage-3 row split) store each row pre-scaled by an exact power of two so its
+// largest magnitude sits in [2^13, 2^14) — inside the fp16 range whatever the
+// input scale (sum-pooled X reaches g·N_q) — and record the
+// inverse power of two here; the product is then exact algebra.
+
 struct GemmEpiParams {
     float* out_f32 = nullptr;  // EPI_F32 / EPI_GELU_PE; resid for EPI_RESID
     __half* out_h = nullptr;   // hi plane
     __half* out_l = nullptr;   // lo plane (nullptr = single plane)
     const float* bias = nullptr;
     const float* pe = nullptr;  // [lw, ldo] fp32
+    const float* row_scale = nullptr;  // [M] power-of-two multipliers (see above)
     int64_t ldo = 0;            // output row stride (elements)
     int64_t lw = 1;             // rows per window (PE period)
 };

@@ -101,6 +101,8 @@ void check_launch(const char* what);
 // ---------------------------------------------------------- kernel entries
 void launch_topk_select(const float* scores, int64_t slices, int64_t n, int64_t k, uint8_t* mask, int32_t* idx,
                         cudaStream_t st);
+void launch_topk_select_f64(const double* scores, int64_t slices, int64_t n, int64_t k, uint8_t* mask, int32_t* idx,
+                            cudaStream_t st);
 void launch_compact_kv(const void* kin, const void* vin, const int32_t* idx, int64_t slices, int64_t n, int64_t k,
                        int64_t row_bytes, void* kout, void* vout, int sm_count, cudaStream_t st);
 // paged destination: slice s's output row j -> page table[s * max_blocks + j / page], row j % page

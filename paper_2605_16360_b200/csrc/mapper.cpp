@@ -488,9 +488,10 @@ void Mapper::run(const float* x, const std::vector<int64_t>& unit_off, int64_t N
     const size_t logit_b = static_cast<size_t>(units * W * hl * Lw) * 4;
     const size_t mean_b = cfg.normalize_input ? static_cast<size_t>(units * W * hs) * 4 : 0;
     const size_t idx_b = (units + W + out_unit.size()) * 8 + 256;
+    const size_t rsc_b = R * 4;  // per-row power-of-two scales of the conv2 / stage-3 A operands
     auto align = [](size_t b) { return (b + 1023) & ~size_t(1023); };
     uint8_t* ws = static_cast<uint8_t*>(work.get(align(z_b) + align(arena_b) + align(logit_b) + align(mean_b) +
-                                                 align(idx_b)));
+                                                 align(idx_b) + align(rsc_b)));
     float* z = reinterpret_cast<float*>(ws);
     uint8_t* arena = ws + align(z_b);
     float* logitsT = reinterpret_cast<float*>(arena + align(arena_b));
@@ -499,6 +500,7 @@ void Mapper::run(const float* x, const std::vector<int64_t>& unit_off, int64_t N
     int64_t* d_unit_off = d_idx;
     int64_t* d_win_off = d_idx + units;
     int* d_out_unit = reinterpret_cast<int*>(d_idx + units + W);
+    float* rscale = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(d_idx) + align(idx_b));
     {
         std::vector<int64_t> h(units + W);
         std::copy(unit_off.begin(), unit_off.end(), h.begin());
@@ -530,13 +532,14 @@ void Mapper::run(const float* x, const std::vector<int64_t>& unit_off, int64_t N
         if (cfg.conv_active) {
             __half* col_h = reinterpret_cast<__half*>(arena);
             __half* col_l = na > 1 ? col_h + rows * 3 * mid : nullptr;
-            launch_conv1_im2col(src, mean, conv1_w, conv1_b, static_cast<int>(mid), col_h, col_l, st);
+            launch_conv1_im2col(src, mean, conv1_w, conv1_b, static_cast<int>(mid), col_h, col_l, rscale, st);
             count_launch(ctx);
             GemmEpiParams p;
             p.out_f32 = z;
             p.ldo = D;
             p.pe = pe_stage1;
             p.lw = Lw;
+            p.row_scale = rscale;
             gemm(col_h, col_l, rows, conv2, conv2_b, pe_stage1 ? EPI_GELU_PE : EPI_GELU_PE, p, st);
         } else {
             launch_bypass_stem(src, mean, bypass_w, bypass_b, pe_stage1, static_cast<int>(D), z, st);
@@ -586,11 +589,12 @@ void Mapper::run(const float* x, const std::vector<int64_t>& unit_off, int64_t N
             __half* zp_h = reinterpret_cast<__half*>(arena);
             __half* zp_l = na > 1 ? zp_h + rows * D : nullptr;
             float* s3 = reinterpret_cast<float*>(zp_h + rows * D * act_planes);
-            launch_split_f16(z, rows * D, zp_h, zp_l, st);
+            launch_split_rows_scaled(z, rows, static_cast<int>(D), zp_h, zp_l, rscale, st);
             count_launch(ctx);
             GemmEpiParams p;
             p.out_f32 = s3;
             p.ldo = ld3;
+            p.row_scale = rscale;
             gemm(zp_h, zp_l, rows, stage3, stage3_b, EPI_F32, p, st);
             launch_stage3(s3, rows, static_cast<int>(ld3), static_cast<int>(hl), static_cast<int>(syn),
                           cfg.cross_active, out_b, static_cast<int>(Lw), logitsT + u0 * W * hl * Lw, st);

@@ -6,6 +6,7 @@
 //                       im2col panel of Stage 1b (conv2 runs as a tcgen05 GEMM)
 //   bypass_stem_kernel  stage_conv = bypass: 1x1 projection (mapper.cpp:302)
 //   layernorm_kernel    pre-norm LN (ops.cpp:721-754) -> fp16 hi/lo planes
+//   split_rows_scaled   Stage-3 input: residual stream -> row-scaled fp16 hi/lo
 //   window_colmean_add  stage_encoder = bypass: z += mean_N z (mapper.cpp:318)
 //   stage3_kernel       Stage 3 on the folded projection: per token, H_l
 //                       softmaxes over the synthetic heads and the value·out_w
@@ -17,11 +18,17 @@
 namespace pkv {
 namespace {
 
-
-__device__ __forceinline__ void store_split(__half* hi, __half* lo, int64_t i, float v) {
-    const __half h = __float2half_rn(v);
-    hi[i] = h;
-    if (lo) lo[i] = __float2half_rn(v - __half2float(h));
+// Power of two s with max_abs·s in [2^13, 2^14) (1 for an all-zero row); the
+// GEMM epilogue multiplies by 1/s (GemmEpiParams::row_scale). Exact: scaling by
+// 2^e only moves the exponent, and 2^14 leaves fp16 headroom for the hi plane's
+// round-up.
+__device__ __forceinline__ float row_pow2_scale(float max_abs) {
+    if (!(max_abs > 0.0f)) return 1.0f;
+    int e;
+    frexpf(max_abs, &e);  // max_abs = m·2^e, m in [0.5, 1)
+    int sh = 14 - e;
+    sh = sh > 100 ? 100 : (sh < -100 ? -100 : sh);
+    return __int_as_float((127 + sh) << 23);
 }
 
 // Source pointer of (unit, window): x + unit_off[unit] + off_w, rows of H_s
@@ -59,14 +66,20 @@ constexpr int kConvTok = 64;  // tokens per block (amortises the per-block weigh
 
 // z1[c, t] = gelu(b1'[c] + Σ_ci Σ_tap W1'[c, ci, tap] · x_pad[ci, t + tap - 1]) (BN folded)
 // im2col row t = [z1[t-1] | z1[t] | z1[t+1]] with zero padding at the window edges.
+// Each panel row is stored pre-scaled by row_pow2_scale(max |row|) and the
+// inverse goes to rinv[row]: sum-pooled X (up to g·N_q) drives z1 far past the
+// fp16 maximum, max-pooled X (<= 1) leaves it tiny; both keep the hi/lo split's
+// full 22-bit precision this way.
 __global__ void conv1_im2col_kernel(WinSrc src, const float* __restrict__ inv_mean, const float* __restrict__ w1,
                                     const float* __restrict__ b1, int mid, __half* __restrict__ col_h,
-                                    __half* __restrict__ col_l) {
+                                    __half* __restrict__ col_l, float* __restrict__ rinv) {
     extern __shared__ float sm[];
     const int hs = src.hs, kw = hs * 3, kws = kw + 1;
     float* sw = sm;                            // [mid][kws]
     float* sx = sw + mid * kws;                // [hs][kConvTok + 4]
     float* sz = sx + hs * (kConvTok + 4);      // [kConvTok + 2][mid]
+    float* smax = sz + (kConvTok + 2) * mid;   // [kConvTok + 2] max |z1| per token
+    float* sscale = smax + (kConvTok + 2);     // [kConvTok] per panel row
     const int uw = blockIdx.y;
     const int u = uw / src.W, w = uw % src.W;
     const int t0 = blockIdx.x * kConvTok;
@@ -97,20 +110,38 @@ __global__ void conv1_im2col_kernel(WinSrc src, const float* __restrict__ inv_me
         }
     }
     __syncthreads();
+    {  // per-token max |z1| (one warp per token), then the per-row scale
+        const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+        for (int tt = warp; tt < kConvTok + 2; tt += nwarps) {
+            float m = 0.0f;
+            for (int c = lane; c < mid; c += 32) m = fmaxf(m, fabsf(sz[tt * mid + c]));
+            for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) smax[tt] = m;
+        }
+    }
+    __syncthreads();
+    const int ntok = min(kConvTok, src.Lw - t0);
+    for (int tt = tid; tt < ntok; tt += blockDim.x) {
+        const float s = row_pow2_scale(fmaxf(fmaxf(smax[tt], smax[tt + 1]), smax[tt + 2]));
+        sscale[tt] = s;
+        rinv[(int64_t)uw * src.Lw + t0 + tt] = 1.0f / s;
+    }
+    __syncthreads();
     const int64_t K = 3 * (int64_t)mid;
     // 16-byte stores: 8 consecutive panel columns (never straddling a tap: mid % 8 == 0)
     const int chunks = (3 * mid) / 8;
-    const int ntok = min(kConvTok, src.Lw - t0);
     for (int i = tid; i < ntok * chunks; i += blockDim.x) {
         const int tt = i / chunks, col = (i % chunks) * 8;
         const int tap = col / mid, c = col % mid;
         const float* zr = sz + (tt + tap) * mid + c;
+        const float s = sscale[tt];
         __align__(16) __half hi[8];
         __align__(16) __half lo[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-            hi[e] = __float2half_rn(zr[e]);
-            lo[e] = __float2half_rn(zr[e] - __half2float(hi[e]));
+            const float v = zr[e] * s;
+            hi[e] = __float2half_rn(v);
+            lo[e] = __float2half_rn(v - __half2float(hi[e]));
         }
         const int64_t off = ((int64_t)uw * src.Lw + t0 + tt) * K + col;
         *reinterpret_cast<uint4*>(col_h + off) = *reinterpret_cast<const uint4*>(hi);
@@ -180,6 +211,51 @@ __global__ void layernorm_kernel(const float* __restrict__ z, int64_t rows, cons
         }
         *reinterpret_cast<uint2*>(hi + row * D + c0) = *reinterpret_cast<const uint2*>(h4);
         if (lo) *reinterpret_cast<uint2*>(lo + row * D + c0) = *reinterpret_cast<const uint2*>(l4);
+    }
+}
+
+// Stage-3 A operand: the raw fp32 residual stream z (no final LN,
+// mapper.cpp:316-324) split into fp16 hi/lo planes, one warp per row, each row
+// pre-scaled by row_pow2_scale(max |row|) with the inverse in rinv[row].
+__global__ void split_rows_scaled_kernel(const float* __restrict__ z, int64_t rows, int D, __half* __restrict__ hi,
+                                         __half* __restrict__ lo, float* __restrict__ rinv) {
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const float* zr = z + row * D;
+    float m = 0.0f;
+    if ((D & 3) == 0) {
+        for (int c = 4 * lane; c < D; c += 128) {
+            const float4 v = *reinterpret_cast<const float4*>(zr + c);
+            m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        }
+    } else {
+        for (int c = lane; c < D; c += 32) m = fmaxf(m, fabsf(zr[c]));
+    }
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float s = row_pow2_scale(m);
+    if (lane == 0) rinv[row] = 1.0f / s;
+    if ((D & 3) == 0) {
+        for (int c = 4 * lane; c < D; c += 128) {
+            const float4 v = *reinterpret_cast<const float4*>(zr + c);
+            const float x[4] = {v.x * s, v.y * s, v.z * s, v.w * s};
+            __align__(8) __half h4[4];
+            __align__(8) __half l4[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                h4[t] = __float2half_rn(x[t]);
+                l4[t] = __float2half_rn(x[t] - __half2float(h4[t]));
+            }
+            *reinterpret_cast<uint2*>(hi + row * D + c) = *reinterpret_cast<const uint2*>(h4);
+            if (lo) *reinterpret_cast<uint2*>(lo + row * D + c) = *reinterpret_cast<const uint2*>(l4);
+        }
+    } else {
+        for (int c = lane; c < D; c += 32) {
+            const float x = zr[c] * s;
+            const __half h = __float2half_rn(x);
+            hi[row * D + c] = h;
+            if (lo) lo[row * D + c] = __float2half_rn(x - __half2float(h));
+        }
     }
 }
 
@@ -261,10 +337,10 @@ void launch_window_mean(const MapperSrc& s, float* mean_out, cudaStream_t st) {
 }
 
 void launch_conv1_im2col(const MapperSrc& s, const float* inv_mean, const float* w1, const float* b1, int mid,
-                         __half* col_h, __half* col_l, cudaStream_t st) {
+                         __half* col_h, __half* col_l, float* rinv, cudaStream_t st) {
     WinSrc w{s.x, s.unit_off, s.win_off, s.head_stride, s.W, s.Lw, s.hs};
     const size_t smem = sizeof(float) * ((size_t)mid * (s.hs * 3 + 1) + (size_t)s.hs * (kConvTok + 4) +
-                                         (size_t)(kConvTok + 2) * mid);
+                                         (size_t)(kConvTok + 2) * mid + (kConvTok + 2) + kConvTok);
     static std::atomic<size_t> attr[64];  // per device (the limit is a per-device function attribute)
     int dev = 0;
     PKV_CUDA(cudaGetDevice(&dev));
@@ -273,7 +349,7 @@ void launch_conv1_im2col(const MapperSrc& s, const float* inv_mean, const float*
         attr[dev & 63] = smem;
     }
     const dim3 grid((unsigned)((s.Lw + kConvTok - 1) / kConvTok), (unsigned)(s.units * s.W));
-    conv1_im2col_kernel<<<grid, 256, smem, st>>>(w, inv_mean, w1, b1, mid, col_h, col_l);
+    conv1_im2col_kernel<<<grid, 256, smem, st>>>(w, inv_mean, w1, b1, mid, col_h, col_l, rinv);
     check_launch("conv1_im2col_kernel");
 }
 
@@ -296,6 +372,13 @@ void launch_layernorm(const float* z, int64_t rows, int D, const float* g, const
         default: throw Error{PKV_ECONFIG, cat("GPU layernorm supports d_time in {128,256,512,1024}, got ", D)};
     }
     check_launch("layernorm_kernel");
+}
+
+void launch_split_rows_scaled(const float* z, int64_t rows, int D, __half* hi, __half* lo, float* rinv,
+                              cudaStream_t st) {
+    if (rows == 0) return;
+    split_rows_scaled_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(z, rows, D, hi, lo, rinv);
+    check_launch("split_rows_scaled_kernel");
 }
 
 void launch_window_colmean_add(float* z, int64_t nwin, int Lw, int D, cudaStream_t st) {

@@ -16,8 +16,11 @@ struct MapperSrc {
 };
 
 void launch_window_mean(const MapperSrc& s, float* mean_out, cudaStream_t st);
+// rinv [rows]: inverse power-of-two scale of each panel row (GemmEpiParams::row_scale)
 void launch_conv1_im2col(const MapperSrc& s, const float* mean, const float* w1, const float* b1, int mid,
-                         __half* col_h, __half* col_l, cudaStream_t st);
+                         __half* col_h, __half* col_l, float* rinv, cudaStream_t st);
+void launch_split_rows_scaled(const float* z, int64_t rows, int D, __half* hi, __half* lo, float* rinv,
+                              cudaStream_t st);
 void launch_bypass_stem(const MapperSrc& s, const float* mean, const float* w, const float* b, const float* pe, int D,
                         float* z, cudaStream_t st);
 void launch_layernorm(const float* z, int64_t rows, int D, const float* g, const float* b, __half* hi, __half* lo,

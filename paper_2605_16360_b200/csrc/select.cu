@@ -6,6 +6,9 @@
 // retained-index lists of apply_mask (proj/src/pruning.cpp:197-215).
 // Order: better(a,b) = v[a] > v[b] || (v[a] == v[b] && a < b)
 // (pruning.cpp:24-31), with -0.0 == +0.0 as in the reference's `!=`.
+// fp32 scores (the device pipeline's Ŷ) use 32-bit order keys; fp64 scores
+// (the reference's ScoreTensor, pkv_topk_select_f64 / pkv_topk_mask_host) use
+// 64-bit keys, so the drop-in ranks arbitrary doubles exactly.
 //
 // One CTA (1024 threads) per slice; HBM-bound: the slice is read once from
 // HBM, the 2 later digit passes and the output pass hit L2 (slices of
@@ -26,6 +29,30 @@ __device__ __forceinline__ uint32_t order_key(float f) {
     if ((u << 1) == 0) u = 0;  // -0.0 -> +0.0
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
+// fp64 scores (the reference's own ScoreTensor type, tensor.hpp:86): the same
+// monotone map on the 64-bit pattern, so distinct doubles never tie.
+__device__ __forceinline__ uint64_t order_key(double f) {
+    uint64_t u = (uint64_t)__double_as_longlong(f);
+    if ((u << 1) == 0) u = 0;
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// Radix digit schedule (most significant first): 12/12/8 bits for 32-bit
+// keys, 12 x 5 + 4 for 64-bit keys.
+template <typename K>
+struct Digits;
+template <>
+struct Digits<uint32_t> {
+    static constexpr int kPasses = 3;
+    __device__ static int bits(int p) { return p < 2 ? 12 : 8; }
+    __device__ static int shift(int p) { return p == 0 ? 20 : (p == 1 ? 8 : 0); }
+};
+template <>
+struct Digits<uint64_t> {
+    static constexpr int kPasses = 6;
+    __device__ static int bits(int p) { return p < 5 ? 12 : 4; }
+    __device__ static int shift(int p) { return p < 5 ? 52 - 12 * p : 0; }
+};
 
 // Block-wide exclusive scan of one uint32 per thread; also returns the total.
 template <int kT = kThreads>
@@ -56,32 +83,40 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* warp_s
     return base + x - v;
 }
 
+// Generic path (rows > 32768 elements, or fp64 scores): the row is re-read
+// per digit pass (L2-resident after the first) instead of register-cached.
+// T: float or double; aligned16 / mask8: the caller's pointers allow the
+// float4 loads / uint2 mask stores.
+template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
-    topk_select_kernel(const float* __restrict__ scores, int64_t n, int64_t k, uint8_t* __restrict__ mask,
-                       int32_t* __restrict__ idx) {
+    topk_select_kernel(const T* __restrict__ scores, int64_t n, int64_t k, uint8_t* __restrict__ mask,
+                       int32_t* __restrict__ idx, bool aligned16, bool mask8) {
+    using Key = decltype(order_key(T(0)));
+    using D = Digits<Key>;
     __shared__ uint32_t hist[4096 + kWarps];  // + one discard bin per warp
     __shared__ uint32_t warp_sums[kWarps];
     __shared__ uint32_t s_digit, s_above;
 
     const int64_t slice = blockIdx.x;
     const uint32_t trash = 4096u + (threadIdx.x >> 5);
-    const float* __restrict__ v = scores + slice * n;
-    const bool vec4 = (n & 3) == 0;
+    const T* __restrict__ v = scores + slice * n;
+    const bool vec4 = sizeof(T) == 4 && aligned16 && (n & 3) == 0;
     const int tid = threadIdx.x;
 
-    // ---- radix select of the k-th largest key: digits of 12, 12 and 8 bits.
-    // Wide first digits spread score rows that share a few exponent values
-    // over many bins (same-bin shared atomics serialise).
-    uint32_t prefix = 0, pmask = 0, kr = (uint32_t)k;
+    // ---- radix select of the k-th largest key. Wide first digits spread
+    // score rows that share a few exponent values over many bins (same-bin
+    // shared atomics serialise).
+    Key prefix = 0, pmask = 0;
+    uint32_t kr = (uint32_t)k;
 #pragma unroll 1
-    for (int pass = 0; pass < 3; ++pass) {
-        const int bits = pass < 2 ? 12 : 8;
-        const int shift = pass == 0 ? 20 : (pass == 1 ? 8 : 0);
+    for (int pass = 0; pass < D::kPasses; ++pass) {
+        const int bits = D::bits(pass);
+        const int shift = D::shift(pass);
         const uint32_t nb = 1u << bits, dmask = nb - 1;
         for (uint32_t j = tid; j < nb; j += kThreads) hist[j] = 0;
         __syncthreads();
-        auto add = [&](uint32_t key) {  // branch-free: non-candidates into the warp's discard bin
-            atomicAdd(&hist[(key & pmask) == prefix ? (key >> shift) & dmask : trash], 1u);
+        auto add = [&](Key key) {  // branch-free: non-candidates into the warp's discard bin
+            atomicAdd(&hist[(key & pmask) == prefix ? (uint32_t)(key >> shift) & dmask : trash], 1u);
         };
         if (vec4) {
             const float4* v4 = reinterpret_cast<const float4*>(v);
@@ -105,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncthreads();
         // thread t owns bins_per_thread consecutive bins in descending digit order
-        const uint32_t bpt = nb / kThreads;  // 4 (12-bit digits) or 0 (8-bit)
+        const uint32_t bpt = nb / kThreads;  // 4 (12-bit digits) or 0 (8/4-bit)
         uint32_t c[4] = {0, 0, 0, 0}, sum = 0;
         if (bpt) {
 #pragma unroll
@@ -131,12 +166,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         __syncthreads();
-        prefix |= s_digit << shift;
-        pmask |= dmask << shift;
+        prefix |= (Key)s_digit << shift;
+        pmask |= (Key)dmask << shift;
         kr -= s_above;
         __syncthreads();
     }
-    const uint32_t kth = prefix;  // key of the k-th best value
+    const Key kth = prefix;          // key of the k-th best value
     const uint32_t ties_taken = kr;  // lowest-index elements with key == kth to keep
 
     // ---- ordered output: mask bits and ascending retained indices
@@ -152,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
             for (int j = 0; j < kItems; ++j) {
-                const uint32_t key = order_key(f[j]);
+                const Key key = order_key(f[j]);
                 gt |= (uint32_t)(key > kth) << j;
                 eq |= (uint32_t)(key == kth) << j;
             }
@@ -160,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < kItems; ++j) {
                 if (i0 + j < n) {
-                    const uint32_t key = order_key(v[i0 + j]);
+                    const Key key = order_key(v[i0 + j]);
                     gt |= (uint32_t)(key > kth) << j;
                     eq |= (uint32_t)(key == kth) << j;
                 }
@@ -186,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         if (mrow) {
-            if ((n & 7) == 0 && i0 + kItems <= n) {
+            if (mask8 && (n & 7) == 0 && i0 + kItems <= n) {
                 uint2 w;
                 w.x = (sel & 1u) | ((sel >> 1) & 1u) << 8 | ((sel >> 2) & 1u) << 16 | ((sel >> 3) & 1u) << 24;
                 w.y = ((sel >> 4) & 1u) | ((sel >> 5) & 1u) << 8 | ((sel >> 6) & 1u) << 16 | ((sel >> 7) & 1u) << 24;
@@ -214,7 +249,7 @@ constexpr int kCacheTiles = 4;
 template <int kT>
 __global__ void __launch_bounds__(kT, 1024 / kT)
     topk_select_cached_kernel(const float* __restrict__ scores, int64_t n, int64_t k, uint8_t* __restrict__ mask,
-                              int32_t* __restrict__ idx) {
+                              int32_t* __restrict__ idx, bool aligned16) {
     __shared__ uint32_t hist[4096 + kT / 32];  // + one discard bin per warp
     __shared__ uint32_t warp_sums[32];
     __shared__ uint32_t s_digit, s_above;
@@ -228,7 +263,7 @@ __global__ void __launch_bounds__(kT, 1024 / kT)
 #pragma unroll
     for (int t = 0; t < kCacheTiles; ++t) {
         const int i0 = t * kT * kItems + tid * kItems;
-        if ((nn & 3) == 0 && i0 + kItems <= nn) {
+        if (aligned16 && (nn & 3) == 0 && i0 + kItems <= nn) {
             const float4 a = __ldcs(reinterpret_cast<const float4*>(v + i0));
             const float4 b = __ldcs(reinterpret_cast<const float4*>(v + i0 + 4));
             key[t][0] = order_key(a.x);
@@ -354,21 +389,33 @@ __global__ void __launch_bounds__(kT, 1024 / kT)
 void launch_topk_select(const float* scores, int64_t slices, int64_t n, int64_t k, uint8_t* mask, int32_t* idx,
                         cudaStream_t st) {
     if (slices == 0) return;
+    // vector loads / stores only where the caller's pointers allow them (a view
+    // with a storage offset, or a row inside a larger buffer, may not)
+    const bool a16 = (reinterpret_cast<uintptr_t>(scores) & 15) == 0;
+    const bool m8 = (reinterpret_cast<uintptr_t>(mask) & 7) == 0;
     // register-cached rows: the smallest CTA that holds the row (more CTAs per
     // SM and shorter block scans for short rows)
     // rows of <= 8192 still take 512 threads: fewer keys per thread shorten the
     // per-slice critical path (8k rows: 22 -> 19 us; one wave of slices either way)
     static const int min_kt = getenv("PKV_SELECT_MIN_THREADS") ? atoi(getenv("PKV_SELECT_MIN_THREADS")) : 512;
     if (n <= 256 * kItems * kCacheTiles && min_kt <= 256) {
-        topk_select_cached_kernel<256><<<(unsigned)slices, 256, 0, st>>>(scores, n, k, mask, idx);
+        topk_select_cached_kernel<256><<<(unsigned)slices, 256, 0, st>>>(scores, n, k, mask, idx, a16);
     } else if (n <= 512 * kItems * kCacheTiles && min_kt <= 512) {
-        topk_select_cached_kernel<512><<<(unsigned)slices, 512, 0, st>>>(scores, n, k, mask, idx);
+        topk_select_cached_kernel<512><<<(unsigned)slices, 512, 0, st>>>(scores, n, k, mask, idx, a16);
     } else if (n <= (int64_t)kThreads * kItems * kCacheTiles) {
-        topk_select_cached_kernel<kThreads><<<(unsigned)slices, kThreads, 0, st>>>(scores, n, k, mask, idx);
+        topk_select_cached_kernel<kThreads><<<(unsigned)slices, kThreads, 0, st>>>(scores, n, k, mask, idx, a16);
     } else {
-        topk_select_kernel<<<(unsigned)slices, kThreads, 0, st>>>(scores, n, k, mask, idx);
+        topk_select_kernel<float><<<(unsigned)slices, kThreads, 0, st>>>(scores, n, k, mask, idx, a16, m8);
     }
     check_launch("topk_select_kernel");
+}
+
+void launch_topk_select_f64(const double* scores, int64_t slices, int64_t n, int64_t k, uint8_t* mask, int32_t* idx,
+                            cudaStream_t st) {
+    if (slices == 0) return;
+    const bool m8 = (reinterpret_cast<uintptr_t>(mask) & 7) == 0;
+    topk_select_kernel<double><<<(unsigned)slices, kThreads, 0, st>>>(scores, n, k, mask, idx, false, m8);
+    check_launch("topk_select_kernel<double>");
 }
 
 }  // namespace pkv

@@ -102,14 +102,15 @@ def topk_select(scores, k: int, *, want_mask: bool = True, want_idx: bool = True
     """Device Top-K: scores fp32 cuda tensor [..., n] -> (mask u8 [..., n] | None, idx i32 [slices, k] | None)."""
     torch = _torch()
     ctx = ctx or Context.default(scores.device.index or 0)
-    if scores.dtype != torch.float32 or not scores.is_cuda:
-        raise ShapeError("topk_select expects a float32 CUDA tensor")
+    if scores.dtype not in (torch.float32, torch.float64) or not scores.is_cuda:
+        raise ShapeError("topk_select expects a float32 or float64 CUDA tensor")
     s = scores.contiguous()
     n = s.shape[-1]
     slices = s.numel() // n if n else 0
     mask = torch.empty(s.shape, dtype=torch.uint8, device=s.device) if want_mask else None
     idx = torch.empty((slices, max(int(k), 0)), dtype=torch.int32, device=s.device) if want_idx else None
-    check(lib().pkv_topk_select(ctx.h, _ptr(s), slices, n, int(k), _ptr(mask), _ptr(idx), _stream(stream)))
+    fn = lib().pkv_topk_select_f64 if s.dtype == torch.float64 else lib().pkv_topk_select
+    check(fn(ctx.h, _ptr(s), slices, n, int(k), _ptr(mask), _ptr(idx), _stream(stream)))
     return mask, idx
 
 
@@ -131,14 +132,17 @@ class PruneMask:
 
 def topk_mask(scores: np.ndarray, rho: float, ctx: Context = None) -> PruneMask:
     """pruning.cpp:37-56 with host scores (the reference signature): GPU radix select,
-    mask bits and ascending indices copied back."""
+    mask bits and ascending indices copied back. fp64 input (the reference's
+    ScoreTensor) is ranked on 64-bit keys, fp32 input on 32-bit keys: exact
+    either way, never narrowed."""
     torch = _torch()
     s = np.asarray(scores)
     if s.ndim == 0:
         raise ShapeError("topk_mask needs a shaped tensor")
     n = s.shape[-1]
     k = retention_count(rho, n)
-    dev = torch.from_numpy(np.ascontiguousarray(s, dtype=np.float32)).cuda()
+    dt = np.float32 if s.dtype == np.float32 else np.float64
+    dev = torch.from_numpy(np.ascontiguousarray(s, dtype=dt)).cuda()
     mask, idx = topk_select(dev, k, ctx=ctx)
     torch.cuda.synchronize()
     return PruneMask(tuple(s.shape), mask.cpu().numpy(), rho, k, idx.cpu().numpy())
