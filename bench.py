@@ -6,15 +6,24 @@ Llama-3.2-1B (proxy) -> Llama-3.1-8B (target) shapes, 32k context, 1 GPU
 (configs[1]); Top-K overlap is measured by the parity tests.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config llama32k|qwen25_128k|qwen25_170k|qwen3_64k|tiny]
+                    [--shard auto|none|layer|head]
 
 A "step" = one full prune of one context: inputs (proxy Q, proxy K, target K/V)
-resident in HBM, outputs = packed K/V + retained indices. `value` = tokens/s
-over all ranks (weak scaling: every rank prunes its own context, no collective
-on the data path). `e2e` = the same through the C-ABI
+resident in HBM, outputs = packed K/V + retained indices. At N = 1 `value` =
+tokens/s of one context on one GPU. Under torchrun (N > 1) the default
+(--shard auto) is STRONG scaling of the same context: the context is split
+across the N GPUs by target layer (configs[2]'s partition; no collective,
+DESIGN.md §7), `value` = N_ctx / (max over ranks of the step time). The N > 1
+line also carries `sharded_configs` (BASELINE configs[2]: Qwen-2.5 170k
+layer-sharded; configs[3]: Qwen-3 64k head-group sharded with the NCCL
+exchange of mapped scores, its time reported) and `weak_scaling` (one
+independent context per GPU). `e2e` = the same metric through the C-ABI
 host-buffer call (pkv_pruner_run_host: H2D of inputs and D2H of outputs inside
-the timed region). `--impl reference` times the reference CPU implementation
-(oracle/_ref, the unmodified reference sources) on the host's cores on a
-bounded sample of the same workload and extrapolates to one context.
+the timed region), all ranks concurrently, max over ranks. `--impl reference`
+times the reference CPU implementation (oracle/_ref, the unmodified reference
+sources) on the host's cores on a bounded sample of the same workload and
+extrapolates to one context.
 """
 from __future__ import annotations
 
@@ -39,6 +48,9 @@ CONFIGS = {
                  desc="tiny synthetic proxy(2L,4H,d64) -> target(4L,8H,d64), N=2048"),
     "qwen25_128k": dict(Ls=24, Hq=14, Hs=2, dp=64, Ll=28, Hl=4, dt=128, N=131072, rho=0.2,
                         desc="Qwen-2.5-0.5B (24L,14Q/2KV,d64) -> Qwen-2.5-7B (28L,4KV,d128), 128k ctx"),
+    "qwen25_170k": dict(Ls=24, Hq=14, Hs=2, dp=64, Ll=28, Hl=4, dt=128, N=170000, rho=0.2,
+                        desc="Qwen-2.5-0.5B (24L,14Q/2KV,d64) -> Qwen-2.5-7B (28L,4KV,d128), 170k ctx "
+                             "(166 windows, right-aligned tail at 167952)"),
     "qwen3_64k": dict(Ls=28, Hq=16, Hs=8, dp=128, Ll=64, Hl=8, dt=128, N=65536, rho=0.2,
                       desc="Qwen-3-0.6B (28L,16Q/8KV,d128) -> Qwen-3-32B (64L,8KV,d128), 64k ctx"),
 }
@@ -165,16 +177,108 @@ def make_inputs(c, device, seed):
 
 
 def time_loop(fn, iters, stream):
+    """Device time per call of `fn` (launches onto `stream`), CUDA events on the
+    launching stream. The launches are queued behind a spin kernel first, so
+    back-to-back kernels are timed, not the host's ctypes / launch overhead
+    (short kernels such as select would otherwise be host-bound)."""
     import torch
     torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(int(2e5 * iters))  # ~0.1 ms per queued call at ~2 GHz
     a.record(stream)
     for _ in range(iters):
         fn()
     b.record(stream)
     torch.cuda.synchronize()
     return a.elapsed_time(b) / iters
+
+
+def max_over_ranks(v, world, dev):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.item()
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def rank_work(c, plan):
+    """Algorithmic work of one rank's part of the context."""
+    pl = plan
+    n_proxy = pl.p_hi - pl.p_lo if pl.b > pl.a else 0
+    score = 2 * flops_score_pass(dict(c, Ls=n_proxy))
+    units = len({(t + 1) * c["Ls"] // c["Ll"] + (1 if ((t + 1) * c["Ls"]) % c["Ll"] else 0) for t in range(pl.a, pl.b)})
+    per_unit = flops_mapper(dict(c, Ll=1, Ls=1))  # one unit's windows
+    slices = (pl.t_hi - pl.t_lo) * (pl.h_hi - pl.h_lo)
+    sel = slices * c["N"] * 4 + slices * k_of(c) * 4
+    cmp = 2 * slices * k_of(c) * c["dt"] * 2 * 2 + slices * k_of(c) * 4
+    return {"proxy_layers": n_proxy, "mapper_units": units, "slices": slices, "score_flop": score,
+            "map_flop": units * per_unit, "select_compact_bytes": sel + cmp}
+
+
+class Arm:
+    """One pruner (sharded or not) for config `c` with its resident inputs."""
+
+    def __init__(self, P, ctx, c, dev, shard, world, rank, precision, seed):
+        import torch
+        self.c = c
+        geom = P.ModelGeometry(c["Ll"], c["Hl"], c["Ls"], c["Hs"], c["dt"])
+        self.mapper = P.Mapper(geom, P.MapperConfig(), seed=7, precision=precision, ctx=ctx)
+        self.comm = None
+        if shard == "none":
+            self.pr = P.Pruner(self.mapper, c["Hq"], c["dp"], c["dt"], c["N"], c["rho"])
+        else:
+            mode = P.SHARD_HEAD if shard == "head" else P.SHARD_LAYER
+            if mode == P.SHARD_HEAD:
+                uid = [P.Comm.unique_id() if rank == 0 else None]
+                if world > 1:
+                    import torch.distributed as dist
+                    dist.broadcast_object_list(uid, src=0)
+                self.comm = P.Comm(ctx, world, rank, uid[0])
+            self.pr = P.Pruner(self.mapper, c["Hq"], c["dp"], c["dt"], c["N"], c["rho"], shard=(mode, world, rank),
+                               comm=self.comm)
+        self.K = K = self.pr.k
+        pl = self.plan = self.pr.plan
+        q, kp, kt, vt = make_inputs(c, dev, seed=seed)
+        self.q, self.kp = q, kp
+        self.kt = kt[pl.t_lo:pl.t_hi, pl.h_lo:pl.h_hi].contiguous()
+        self.vt = vt[pl.t_lo:pl.t_hi, pl.h_lo:pl.h_hi].contiguous()
+        del kt, vt
+        nt, nh = pl.t_hi - pl.t_lo, pl.h_hi - pl.h_lo
+        self.ko = torch.empty(nt, nh, K, c["dt"], dtype=torch.bfloat16, device=dev)
+        self.vo = torch.empty_like(self.ko)
+        self.idx = torch.empty(nt, nh, K, dtype=torch.int32, device=dev)
+
+    def step(self, stream):
+        self.pr.run(self.q, self.kp, self.kt, self.vt, self.ko, self.vo, self.idx, stream=stream)
+
+    def timed(self, steps, warmup, stream, world, dev):
+        """max over ranks of the per-step device time (barrier + sync around)."""
+        import torch
+        for _ in range(warmup):
+            self.step(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            self.step(stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / steps
+        barrier(world)
+        return ms, max_over_ranks(ms, world, dev)
 
 
 def run_ours(args, c, rank, world, local_rank):
@@ -187,83 +291,132 @@ def run_ours(args, c, rank, world, local_rank):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     ctx = P.Context(local_rank)
-    geom = P.ModelGeometry(c["Ll"], c["Hl"], c["Ls"], c["Hs"], c["dt"])
-    mcfg = P.MapperConfig()
-    mapper = P.Mapper(geom, mcfg, seed=7, precision=args.precision, ctx=ctx)
-    comm = None
-    if args.shard == "none":
-        pr = P.Pruner(mapper, c["Hq"], c["dp"], c["dt"], c["N"], c["rho"])
-        seed = 1234 + rank  # weak scaling: an independent context per rank
-    else:
-        mode = P.SHARD_HEAD if args.shard == "head" else P.SHARD_LAYER
-        if mode == P.SHARD_HEAD:
-            uid = [P.Comm.unique_id() if rank == 0 else None]
-            if world > 1:
-                import torch.distributed as dist
-                dist.broadcast_object_list(uid, src=0)
-            comm = P.Comm(ctx, world, rank, uid[0])
-        pr = P.Pruner(mapper, c["Hq"], c["dp"], c["dt"], c["N"], c["rho"], shard=(mode, world, rank), comm=comm)
-        seed = 1234  # strong scaling: every rank holds its part of the same context
-    K = pr.k
-    pl = pr.plan
-    q, kp, kt, vt = make_inputs(c, dev, seed=seed)
-    kt = kt[pl.t_lo:pl.t_hi, pl.h_lo:pl.h_hi].contiguous()
-    vt = vt[pl.t_lo:pl.t_hi, pl.h_lo:pl.h_hi].contiguous()
-    nt, nh = pl.t_hi - pl.t_lo, pl.h_hi - pl.h_lo
-    ko = torch.empty(nt, nh, K, c["dt"], dtype=torch.bfloat16, device=dev)
-    vo = torch.empty_like(ko)
-    idx = torch.empty(nt, nh, K, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
-    step = lambda: pr.run(q, kp, kt, vt, ko, vo, idx, stream=stream)
+    shard = args.shard if args.shard != "auto" else ("layer" if world > 1 else "none")
+    # weak scaling replicas: an independent context per rank; sharded: every
+    # rank holds its part of the same context
+    arm = Arm(P, ctx, c, dev, shard, world, rank, args.precision, 1234 + (rank if shard == "none" else 0))
 
     for _ in range(args.warmup):
-        step()
+        arm.step(stream)
     torch.cuda.synchronize()
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
+    barrier(world)
     torch.cuda.synchronize()
     l0 = ctx.launches()
     with ClockSampler(local_rank) as clk:
-        ms = time_loop(step, args.steps, stream)
-    launches = (ctx.launches() - l0) // max(args.steps, 1) * args.steps
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            arm.step(stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+    ms_rank = a.elapsed_time(b) / args.steps
+    launches = ctx.launches() - l0
+    barrier(world)
+    ms = max_over_ranks(ms_rank, world, dev)
+
+    result = {"ms": ms, "K": arm.K, "launches": launches, "clocks": clk.summary(), "shard": shard}
+    work = rank_work(c, arm.plan)
+    per_rank = {"rank": rank, "ms": ms_rank, **work,
+                "score_map_TFLOP/s": (work["score_flop"] + work["map_flop"]) / (ms_rank * 1e-3) / 1e12}
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
-        dist.barrier()
-
-    result = {"ms": ms, "K": K, "launches": launches, "clocks": clk.summary()}
-    if rank == 0:
-        if args.shard == "none":
-            result["stages"] = stage_breakdown(P, ctx, mapper, c, q, kp, kt, vt, ko, vo, K, stream, args)
-        if not args.no_e2e:
-            result["e2e"] = e2e(P, pr, c, K, args)
+        allr = [None] * world
+        dist.all_gather_object(allr, per_rank)
+        result["per_rank"] = allr
+    if rank == 0 and world == 1:
+        result["stages"] = stage_breakdown(P, ctx, arm, c, stream, args)
+    if not args.no_e2e:
+        e = e2e(P, arm, c, args, world, dev)
+        if rank == 0:
+            result["e2e"] = e
+    del arm
+    torch.cuda.empty_cache()
+    if world > 1 and not args.no_extras:
+        result["weak_scaling"] = weak_scaling(P, ctx, c, dev, world, rank, args, stream)
+        result["sharded_configs"] = sharded_configs(P, ctx, dev, world, rank, args, stream)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
     return result
 
 
-def stage_breakdown(P, ctx, mapper, c, q, kp, kt, vt, ko, vo, K, stream, args):
+def weak_scaling(P, ctx, c, dev, world, rank, args, stream):
     import torch
-    it = max(2, min(args.steps, 5))
-    lse = P.score_lse(q, kp, ctx=ctx)
-    x = torch.empty(c["Ls"], c["Hs"], c["N"], device=q.device)
-    y = torch.empty(1, c["Ll"], c["Hl"], c["N"], device=q.device)
-    idx = torch.empty(c["Ll"] * c["Hl"], K, dtype=torch.int32, device=q.device)
+    arm = Arm(P, ctx, c, dev, "none", world, rank, args.precision, 1234 + rank)
+    _, ms = arm.timed(max(2, min(args.steps, 5)), 3, stream, world, dev)
+    del arm
+    torch.cuda.empty_cache()
+    return {"value": world * c["N"] / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+            "note": f"{world} independent {c['N']}-token contexts, one per GPU, no collective"}
+
+
+def sharded_configs(P, ctx, dev, world, rank, args, stream):
+    """BASELINE configs[2] (Qwen-2.5 170k, layer-sharded) and configs[3]
+    (Qwen-3 64k, head-group sharded: NCCL all-to-all of mapped scores) as
+    strong scaling of one context over the `world` GPUs."""
+    import torch
     out = {}
-    out["score_lse_ms"] = time_loop(lambda: P.score_lse(q, kp, ctx=ctx, stream=stream), it, stream)
-    out["score_pool_ms"] = time_loop(lambda: P.score(q, kp, lse=lse, ctx=ctx, stream=stream, out=x), it, stream)
-    out["map_ms"] = time_loop(lambda: mapper.forward_full(x.view(1, *x.shape), stream=stream, out=y), it, stream)
-    ys = y.view(-1, c["N"])
-    out["select_ms"] = time_loop(lambda: P.topk_select(ys, K, want_mask=False, ctx=ctx, stream=stream), it, stream)
-    _, idx = P.topk_select(ys, K, want_mask=False, ctx=ctx, stream=stream)
+    for name, mode in (("qwen25_170k", "layer"), ("qwen3_64k", "head")):
+        cc = CONFIGS[name]
+        if (mode == "layer" and world > cc["Ll"]) or (mode == "head" and world > cc["Hl"]):
+            continue
+        arm = Arm(P, ctx, cc, dev, mode, world, rank, args.precision, 1234)
+        ms_rank, ms = arm.timed(max(2, min(args.steps, 3)), 3, stream, world, dev)
+        rec = {"shard": mode, "N": cc["N"], "ms_per_context": ms, "tokens_per_s": cc["N"] / (ms * 1e-3),
+               "desc": cc["desc"]}
+        work = rank_work(cc, arm.plan)
+        allr = [None] * world
+        import torch.distributed as dist
+        dist.all_gather_object(allr, {"rank": rank, "ms": ms_rank, **work,
+                                      "score_map_TFLOP/s": (work["score_flop"] + work["map_flop"]) /
+                                                           (ms_rank * 1e-3) / 1e12})
+        rec["per_rank"] = allr
+        if mode == "head":
+            pl = arm.plan
+            y_local = torch.zeros(max(pl.b - pl.a, 1), cc["Hl"], cc["N"], device=dev)
+            y_recv = torch.zeros(cc["Ll"], pl.h_hi - pl.h_lo, cc["N"], device=dev)
+            barrier(world)
+            x_ms = time_loop(lambda: arm.pr.exchange(y_local, y_recv, stream=stream), 5, stream)
+            rec["exchange_ms"] = max_over_ranks(x_ms, world, dev)
+            rec["exchange_bytes_total"] = cc["Ll"] * cc["Hl"] * cc["N"] * 4
+        del arm
+        torch.cuda.empty_cache()
+        out[name] = rec
+    return out
+
+
+def stage_breakdown(P, ctx, arm, c, stream, args):
+    """Each stage alone through the C ABI with preallocated outputs, timed as
+    back-to-back launches (time_loop)."""
+    import torch
+    L = P.lib()
+    q, kp, kt, vt, ko, vo, K = arm.q, arm.kp, arm.kt, arm.vt, arm.ko, arm.vo, arm.K
+    sp = stream.cuda_stream
+    it = max(3, min(args.steps, 5))
+    dev = q.device
+    lse = torch.empty(c["Ls"], c["Hq"], c["N"], device=dev)
+    x = torch.empty(c["Ls"], c["Hs"], c["N"], device=dev)
+    y = torch.empty(1, c["Ll"], c["Hl"], c["N"], device=dev)
     S = c["Ll"] * c["Hl"]
-    out["compact_ms"] = time_loop(
-        lambda: P.compact_kv(kt.view(S, c["N"], c["dt"]), vt.view(S, c["N"], c["dt"]), idx, ctx=ctx, stream=stream,
-                             out=(ko.view(S, K, c["dt"]), vo.view(S, K, c["dt"]))), it, stream)
+    idx = torch.empty(S, K, dtype=torch.int32, device=dev)
+    dims = (c["Ls"], c["Hq"], c["Hs"], c["N"], c["N"], c["dp"])
+    lse_call = lambda: P.check(L.pkv_score_lse(ctx.h, q.data_ptr(), kp.data_ptr(), *dims, 0, lse.data_ptr(), sp))
+    pool_call = lambda: P.check(L.pkv_score(ctx.h, q.data_ptr(), kp.data_ptr(), *dims, P.SCORE_REDUCE_MAX,
+                                            lse.data_ptr(), x.data_ptr(), sp))
+    map_call = lambda: P.check(L.pkv_mapper_forward_full(arm.mapper.h, x.data_ptr(), 1, c["N"], y.data_ptr(), sp))
+    sel_call = lambda: P.check(L.pkv_topk_select(ctx.h, y.data_ptr(), S, c["N"], K, None, idx.data_ptr(), sp))
+    cmp_call = lambda: P.check(L.pkv_compact_kv(ctx.h, kt.data_ptr(), vt.data_ptr(), idx.data_ptr(), S, c["N"], K,
+                                                c["dt"], 2, ko.data_ptr(), vo.data_ptr(), sp))
+    for f in (lse_call, pool_call, map_call, sel_call, cmp_call):
+        f()
+    out = {}
+    out["score_lse_ms"] = time_loop(lse_call, it, stream)
+    out["score_pool_ms"] = time_loop(pool_call, it, stream)
+    out["map_ms"] = time_loop(map_call, it, stream)
+    out["select_ms"] = time_loop(sel_call, 20, stream)
+    out["compact_ms"] = time_loop(cmp_call, 10, stream)
     # SURVEY §8(f)-1: causal scoring with the LSE emitted by the proxy's own prefill
     # attention (its O is the proxy model's output anyway): one scoring pass
     vp = torch.randn_like(kp)
@@ -273,34 +426,43 @@ def stage_breakdown(P, ctx, mapper, c, q, kp, kt, vt, ko, vo, K, stream, args):
     out["x_score_pool_causal_ms"] = time_loop(
         lambda: P.score(q, kp, lse=plse, causal=True, ctx=ctx, stream=stream, out=x), it, stream)
     # the whole prune in that regime: causal pruner fed the prefill LSE (pkv_pruner_run_lse)
-    prc = P.Pruner(mapper, c["Hq"], c["dp"], c["dt"], c["N"], c["rho"], causal=True)
+    prc = P.Pruner(arm.mapper, c["Hq"], c["dp"], c["dt"], c["N"], c["rho"], causal=True)
     prc.run_lse(q, kp, plse, kt, vt, ko, vo, stream=stream)
     out["x_prune_with_prefill_lse_ms"] = time_loop(lambda: prc.run_lse(q, kp, plse, kt, vt, ko, vo, stream=stream),
                                                    it, stream)
     return out
 
 
-def e2e(P, pr, c, K, args):
+def e2e(P, arm, c, args, world, dev):
+    """The public host-buffer call on every rank at once (pinned host inputs in,
+    packed K/V + indices out, copies inside the timed region); max over ranks."""
     import torch
-    pl = pr.plan
-    q, kp, kt, vt = make_inputs(c, torch.device("cuda"), seed=99)
+    pl = arm.plan
+    q, kp, kt, vt = make_inputs(c, dev, seed=99)
     kt = kt[pl.t_lo:pl.t_hi, pl.h_lo:pl.h_hi]
     vt = vt[pl.t_lo:pl.t_hi, pl.h_lo:pl.h_hi]
     q, kp, kt, vt = (t.contiguous().cpu().pin_memory() for t in (q, kp, kt, vt))
     nt, nh = pl.t_hi - pl.t_lo, pl.h_hi - pl.h_lo
+    K = arm.K
     ko = torch.empty(nt, nh, K, c["dt"], dtype=torch.bfloat16).pin_memory()
     vo = torch.empty_like(ko).pin_memory()
     idx = torch.empty(nt, nh, K, dtype=torch.int32).pin_memory()
     stream = torch.cuda.current_stream()
-    step = lambda: pr.run_host(q, kp, kt, vt, ko, vo, idx, stream=stream)
+    step = lambda: arm.pr.run_host(q, kp, kt, vt, ko, vo, idx, stream=stream)
     for _ in range(max(1, min(args.warmup, 2))):
         step()
     n = max(2, min(args.steps, 5))
+    torch.cuda.synchronize()
+    barrier(world)
     t0 = time.perf_counter()
     for _ in range(n):
         step()  # synchronises on the stream at the end of every call
     ms = (time.perf_counter() - t0) * 1e3 / n
-    h2d = sum(t.numel() * t.element_size() for t in (q, kp, kt, vt))
+    ms = max_over_ranks(ms, world, dev)
+    # bytes this rank moves: the proxy layers its pruner reads + its KV shard in, its outputs back
+    Ls = c["Ls"]
+    read_layers = (pl.p_hi - pl.p_lo) if pl.b > pl.a else 0
+    h2d = (q.numel() * 2 + kp.numel() * 2) * read_layers // Ls + (kt.numel() + vt.numel()) * 2
     d2h = sum(t.numel() * t.element_size() for t in (ko, vo, idx))
     return {"ms": ms, "h2d": h2d, "d2h": d2h}
 
@@ -372,14 +534,43 @@ def cpu_sample_desc(c, threads):
             f"(no reference code for those), extrapolated to one {c['N']}-token context")
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_legs(c, st, threads):
+    """Which stage times are the reference's own code and which are the C
+    restatement (no reference code), and how each was extrapolated."""
+    U, W = unique_pairs(c["Ll"], c["Ls"]), windows(c["N"])
+    return {
+        "select": {"s": st["select"], "code": "reference (topk_mask + apply_mask, pruning.cpp)",
+                   "extrapolated": f"1 of {c['Ll']} target layers timed, x{c['Ll']}"},
+        "map": {"s": st["map"], "code": "reference (forward_pair, mapper.cpp)",
+                "extrapolated": f"{threads} windows timed concurrently on {threads} cores, x ceil({U}*{W}/{threads})"},
+        "score": {"s": st["score"], "code": "C restatement (SPEC-only scoring, no reference code)",
+                  "extrapolated": f"{threads} (layer, kv-head, 256-query) blocks, x N/256*L_s*H_s/{threads}"},
+        "compact": {"s": st["compact"], "code": "C restatement (the reference has no gather)",
+                    "extrapolated": f"1 of {c['Ll']} target layers, x{c['Ll']}"},
+    }
+
+
 def run_reference(args, c):
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):  # warm-up: the cheap stages only
         cpu_reference_sample(c, threads, include_mapper=False)
     totals = []
+    t_wall = time.perf_counter()
     for _ in range(args.steps):
         st = cpu_reference_sample(c, threads)
         totals.append(sum(st.values()))
+    t_wall = time.perf_counter() - t_wall
     sec = statistics.mean(totals)
     value = c["N"] / sec
     return {
@@ -387,8 +578,10 @@ def run_reference(args, c):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "desc": c["desc"], "rho": c["rho"], "N": c["N"]},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": cpu_sample_desc(c, threads), "stage_s": st},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(),
+                         "kind": "reference", "sample": cpu_sample_desc(c, threads), "extrapolated": True,
+                         "timed_wall_s_per_step": t_wall / max(args.steps, 1),
+                         "stage_s": {k: round(v, 3) for k, v in st.items()}, "legs": cpu_legs(c, st, threads)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -404,15 +597,19 @@ def main():
     ap.add_argument("--precision", type=int, default=3, help="mapper precision mode (1 fp16, 2 act split, 3 act+wt split)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--shard", choices=["none", "layer", "head"], default="none",
-                    help="none: weak scaling (one independent context per GPU); layer/head: one context split "
-                         "across the GPUs (strong scaling; head = NCCL exchange of mapped scores)")
+    ap.add_argument("--no-extras", action="store_true", help="N > 1: skip weak_scaling and sharded_configs")
+    ap.add_argument("--shard", choices=["auto", "none", "layer", "head"], default="auto",
+                    help="auto: none at N = 1, layer at N > 1 (strong scaling of one context); none: weak scaling "
+                         "(one independent context per GPU); head: head-group sharding with the NCCL exchange")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     c = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator / NVLS setup to stderr
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 
     if args.impl == "reference":
         if rank == 0:
@@ -427,15 +624,16 @@ def main():
         return
     hbm, tf_burst, tf_sus, src = peaks()
     ms = r["ms"]
-    sharded = args.shard != "none"
+    sharded = r["shard"] != "none"
+    n_ctx = 1 if sharded else world
     line = {
-        "metric": METRIC, "value": c["N"] * (1 if sharded else world) / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        "metric": METRIC, "value": c["N"] * n_ctx / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": args.config, "desc": c["desc"], "rho": c["rho"], "N": c["N"], "K": r["K"],
                    "mapper_precision": args.precision, "score_reduce": "max", "score_passes": 2,
-                   "l2": "inputs (7 GB) > L2 (126 MB); no explicit flush",
-                   "parallelism": (f"{args.shard}-sharded: one context over {world} GPUs" if sharded
+                   "l2": "inputs (>= 7 GB) > L2 (126 MB); no explicit flush",
+                   "parallelism": (f"{r['shard']}-sharded: one context over {world} GPUs" if sharded
                                    else f"weak: {world} independent contexts, one per GPU")},
         "prune_latency_ms": ms,
     }
@@ -476,6 +674,8 @@ def main():
         sc_b = bytes_select(c) + bytes_compact(c)
         sc_ms = st["select_ms"] + st["compact_ms"]
         line["stages_ms"] = {k[:-3]: v for k, v in st.items() if not k.startswith("x_")}
+        line["stages_note"] = ("each stage alone through the C ABI with preallocated outputs, back-to-back launches "
+                               "queued behind a spin kernel (device time, not host launch overhead)")
         fc = 2 * c["dp"] * (c["N"] * (c["N"] + 1) // 2) * c["Hq"] * c["Ls"]  # causal pairs
         line["scoring_single_pass"] = {
             "note": "causal scoring with the LSE from the proxy's prefill attention (pkv_proxy_prefill_attention, "
@@ -489,24 +689,33 @@ def main():
             "score_lse": {"TFLOP/s": flops_score_pass(c) / st["score_lse_ms"] / 1e9},
             "score_pool": {"TFLOP/s": flops_score_pass(c) / st["score_pool_ms"] / 1e9},
             "map": {"TFLOP/s": flops_mapper(c) / st["map_ms"] / 1e9},
+            "select": {"GB/s": bytes_select(c) / st["select_ms"] / 1e6,
+                       "frac_hbm": bytes_select(c) / st["select_ms"] / 1e6 / hbm},
+            "compact": {"GB/s": bytes_compact(c) / st["compact_ms"] / 1e6,
+                        "frac_hbm": bytes_compact(c) / st["compact_ms"] / 1e6 / hbm},
             "select+compact": {"GB/s": sc_b / sc_ms / 1e6, "frac_hbm": sc_b / sc_ms / 1e6 / hbm},
         }
         line["roofline"] = roof
+    for key in ("per_rank", "weak_scaling", "sharded_configs"):
+        if key in r:
+            line[key] = r[key]
     line["clocks"] = r["clocks"]
     line["gpu_launches"] = r["launches"]
     if "e2e" in r:
         e = r["e2e"]
-        line["e2e"] = {"value": c["N"] * (1 if sharded else world) / (e["ms"] * 1e-3), "unit": UNIT,
+        line["e2e"] = {"value": c["N"] * n_ctx / (e["ms"] * 1e-3), "unit": UNIT,
                        "h2d_bytes_per_step": e["h2d"], "d2h_bytes_per_step": e["d2h"], "ms_per_step": e["ms"],
-                       "note": "pkv_pruner_run_host on rank 0 (wall clock, synchronised per call)"}
+                       "note": "pkv_pruner_run_host on every rank at once (wall clock, synchronised per call, max over "
+                               "ranks); bytes are rank 0's"}
     if not args.no_cpu_baseline and world == 1:
         try:
             threads = os.cpu_count() or 1
             stc = cpu_reference_sample(c, threads)
             sec = sum(stc.values())
-            line["cpu_baseline"] = {"value": c["N"] / sec, "unit": UNIT, "cores": threads, "kind": "reference",
-                                    "sample": cpu_sample_desc(c, threads),
-                                    "stage_s": {k: round(v, 3) for k, v in stc.items()}}
+            line["cpu_baseline"] = {"value": c["N"] / sec, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(),
+                                    "kind": "reference", "sample": cpu_sample_desc(c, threads), "extrapolated": True,
+                                    "stage_s": {k: round(v, 3) for k, v in stc.items()},
+                                    "legs": cpu_legs(c, stc, threads)}
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "unavailable": f"{type(e).__name__}: {e}"}
     print(json.dumps(line))

@@ -369,6 +369,20 @@ pkv_status pkv_pruner_create_sharded(pkv_ctx ctx, pkv_mapper m, int64_t Hq, int6
                                      double rho, uint32_t score_flags, uint32_t shard_mode, int world, int rank,
                                      pkv_comm comm, pkv_pruner* out);
 
+/* The head-group exchange as a list of point-to-point operations (host logic
+ * only; the NCCL exchange inside a PKV_SHARD_HEAD pruner issues exactly these,
+ * in this order, inside one ncclGroupStart/End). Each op is 5 int64:
+ *   {kind (0 send, 1 recv), peer rank, element offset, element count, tag}
+ * sends read y_local [b-a, H_l, N] (this rank's mapped target layers, all
+ * heads), recvs write y_recv [L_l, h_hi-h_lo, N] (every target layer, this
+ * rank's heads); tag = the target layer, so (peer, tag) matches a send with
+ * its recv. count_out = number of ops (all of them, even past cap). */
+pkv_status pkv_shard_exchange_schedule(const int64_t* geom5, int world, int rank, int64_t N, int64_t* ops_out,
+                                       int64_t cap, int64_t* count_out);
+/* Runs a head-group pruner's exchange alone on `stream` (y_local / y_recv as
+ * above): the step pkv_pruner_run performs between mapping and select. */
+pkv_status pkv_pruner_exchange(pkv_pruner p, const float* y_local_dev, float* y_recv_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -116,6 +116,9 @@ SIGNATURES = {
     "pkv_packed_decode_attention": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp] + [_c_i64] * 5 + [_c_dbl, _c_vp,
                                                                                                 _c_vp]),
     "pkv_shard_plan": (ctypes.c_int, [_c_i64p, ctypes.c_int, ctypes.c_int, _c_u32, _c_i64p]),
+    "pkv_shard_exchange_schedule": (ctypes.c_int, [_c_i64p, ctypes.c_int, ctypes.c_int, _c_i64, _c_vp, _c_i64,
+                                                   _c_i64p]),
+    "pkv_pruner_exchange": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp]),
     "pkv_trace_write": (ctypes.c_int, [ctypes.c_char_p, _c_i64p, _c_i64, _c_vp, _c_vp, ctypes.c_char_p]),
     "pkv_trace_read_header": (ctypes.c_int, [ctypes.c_char_p, _c_i64p, _c_i64p]),
     "pkv_trace_read": (ctypes.c_int, [ctypes.c_char_p, _c_vp, _c_vp]),

@@ -252,6 +252,15 @@ pkv_status pkv_pruner_run(pkv_pruner p, const void* q, const void* kp, const voi
     });
 }
 
+pkv_status pkv_pruner_exchange(pkv_pruner p, const float* y_local_dev, float* y_recv_dev, void* stream) {
+    return guard([&] {
+        PKV_REQUIRE_VALUE(p != nullptr, "null pkv_pruner");
+        PKV_REQUIRE_VALUE(p->plan.mode == PKV_SHARD_HEAD && p->comm != nullptr,
+                          "pkv_pruner_exchange needs a head-group sharded pruner");
+        exchange_scores(p->comm, p->plan, p->Hl, p->N, y_local_dev, y_recv_dev, static_cast<cudaStream_t>(stream));
+    });
+}
+
 pkv_status pkv_pruner_run_lse(pkv_pruner p, const void* q, const void* kp, const float* lse, const void* kt,
                               const void* vt, void* k_out, void* v_out, int32_t* idx_out, float* scores_out,
                               void* stream) {

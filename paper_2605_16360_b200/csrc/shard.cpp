@@ -134,24 +134,34 @@ ShardPlan make_shard_plan(const Geometry& g, int world, int rank, uint32_t mode)
     return p;
 }
 
-void exchange_scores(pkv_comm comm, const ShardPlan& plan, int64_t Hl, int64_t N, const float* y_local,
-                     float* y_recv, cudaStream_t st) {
-    const Nccl& n = nccl();
-    auto c = static_cast<ncclComm_t>(comm->nccl);
+std::vector<XOp> exchange_schedule(const ShardPlan& plan, int64_t Hl, int64_t N) {
+    std::vector<XOp> ops;
+    if (plan.mode != PKV_SHARD_HEAD) return ops;
     const int64_t nh = plan.h_hi - plan.h_lo;
-    nccl_check(n.group_start(), "ncclGroupStart");
     for (int64_t t = plan.a; t < plan.b; ++t) {
         for (int g = 0; g < plan.world; ++g) {
             const int64_t hg = plan.h_begin[g], ng = plan.h_begin[g + 1] - hg;
             if (ng == 0) continue;
-            nccl_check(n.send(y_local + ((t - plan.a) * Hl + hg) * N, static_cast<size_t>(ng * N), ncclFloat, g, c, st),
-                       "ncclSend");
+            ops.push_back({0, g, ((t - plan.a) * Hl + hg) * N, ng * N, t});
         }
     }
     if (nh > 0) {
         for (int64_t t = 0; t < static_cast<int64_t>(plan.producer.size()); ++t)
-            nccl_check(n.recv(y_recv + t * nh * N, static_cast<size_t>(nh * N), ncclFloat, plan.producer[t], c, st),
-                       "ncclRecv");
+            ops.push_back({1, plan.producer[t], t * nh * N, nh * N, t});
+    }
+    return ops;
+}
+
+void exchange_scores(pkv_comm comm, const ShardPlan& plan, int64_t Hl, int64_t N, const float* y_local,
+                     float* y_recv, cudaStream_t st) {
+    const Nccl& n = nccl();
+    auto c = static_cast<ncclComm_t>(comm->nccl);
+    nccl_check(n.group_start(), "ncclGroupStart");
+    for (const XOp& op : exchange_schedule(plan, Hl, N)) {
+        if (op.kind == 0)
+            nccl_check(n.send(y_local + op.off, static_cast<size_t>(op.count), ncclFloat, op.peer, c, st), "ncclSend");
+        else
+            nccl_check(n.recv(y_recv + op.off, static_cast<size_t>(op.count), ncclFloat, op.peer, c, st), "ncclRecv");
     }
     nccl_check(n.group_end(), "ncclGroupEnd");
 }
@@ -167,6 +177,21 @@ pkv_status pkv_shard_plan(const int64_t* geom5, int world, int rank, uint32_t mo
         const ShardPlan p = make_shard_plan(Geometry::from5(geom5), world, rank, mode);
         const int64_t v[8] = {p.t_lo, p.t_hi, p.h_lo, p.h_hi, p.p_lo, p.p_hi, p.a, p.b};
         for (int i = 0; i < 8; ++i) out8[i] = v[i];
+    });
+}
+
+pkv_status pkv_shard_exchange_schedule(const int64_t* geom5, int world, int rank, int64_t N, int64_t* ops_out,
+                                       int64_t cap, int64_t* count_out) {
+    return guard([&] {
+        PKV_REQUIRE_VALUE(N > 0, "context length must be positive");
+        const Geometry g = Geometry::from5(geom5);
+        const auto ops = exchange_schedule(make_shard_plan(g, world, rank, PKV_SHARD_HEAD), g.target_heads, N);
+        *count_out = static_cast<int64_t>(ops.size());
+        for (int64_t i = 0; i < cap && i < *count_out; ++i) {
+            const XOp& o = ops[i];
+            const int64_t v[5] = {o.kind, o.peer, o.off, o.count, o.tag};
+            for (int j = 0; j < 5; ++j) ops_out[i * 5 + j] = v[j];
+        }
     });
 }
 

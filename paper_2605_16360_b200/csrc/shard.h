@@ -30,6 +30,17 @@ struct ShardPlan {
 
 ShardPlan make_shard_plan(const Geometry& g, int world, int rank, uint32_t mode);
 
+// One point-to-point operation of the head-group exchange.
+struct XOp {
+    int kind;      // 0 send (from y_local), 1 recv (into y_recv)
+    int peer;
+    int64_t off;   // element offset into y_local / y_recv
+    int64_t count; // elements
+    int64_t tag;   // target layer
+};
+// The exchange as ops, in issue order (sends, then recvs).
+std::vector<XOp> exchange_schedule(const ShardPlan& plan, int64_t Hl, int64_t N);
+
 // NCCL point-to-point exchange of mapped scores (head mode): rank r sends
 // y_local[t - a, heads of g, :] to every g for its produced layers t, and
 // receives y_recv[t, :, :] (its own head group) from producer(t) for all t.

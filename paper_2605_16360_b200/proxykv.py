@@ -29,7 +29,7 @@ __all__ = [
     "layer_pair", "window_offsets", "mapper_init_params", "ShapeError", "PkvValueError", "ConfigError",
     "CudaError", "NoDeviceError", "PkvError", "SCORE_REDUCE_MAX", "SCORE_REDUCE_SUM", "SCORE_CAUSAL",
     "MAPPER_FP16", "MAPPER_FP16X2", "MAPPER_FP16X3", "SHARD_LAYER", "SHARD_HEAD", "ShardPlan", "shard_plan",
-    "Comm", "write_trace", "read_trace", "write_checkpoint", "read_checkpoint", "IoError", "BadMagicError",
+    "Comm", "shard_exchange_schedule", "write_trace", "read_trace", "write_checkpoint", "read_checkpoint", "IoError", "BadMagicError",
     "VersionMismatchError", "TruncatedFileError", "PayloadLengthError",
 ]
 
@@ -602,6 +602,18 @@ def shard_plan(geom: ModelGeometry, world: int, rank: int, mode: int = SHARD_LAY
     return ShardPlan(*[int(v) for v in out])
 
 
+def shard_exchange_schedule(geom: ModelGeometry, world: int, rank: int, N: int) -> np.ndarray:
+    """The head-group exchange of rank `rank` as int64 ops [n, 5] = (kind 0 send / 1 recv, peer,
+    element offset, element count, tag = target layer) — exactly what the NCCL exchange issues
+    (pkv_shard_exchange_schedule; host logic only)."""
+    cnt = ctypes.c_int64()
+    check(lib().pkv_shard_exchange_schedule(geom.as5(), world, rank, N, None, 0, ctypes.byref(cnt)))
+    ops = np.zeros((max(cnt.value, 1), 5), np.int64)
+    check(lib().pkv_shard_exchange_schedule(geom.as5(), world, rank, N, ops.ctypes.data, cnt.value,
+                                            ctypes.byref(cnt)))
+    return ops[:cnt.value]
+
+
 class Comm:
     """pkv_comm: NCCL communicator for head-group sharding. `uid` is the
     PKV_COMM_ID_BYTES id from Comm.unique_id() on rank 0, distributed by the
@@ -663,6 +675,10 @@ class Pruner:
     def run(self, q, kp, kt, vt, k_out, v_out, idx_out=None, scores_out=None, stream=None):
         check(lib().pkv_pruner_run(self.h, _ptr(q), _ptr(kp), _ptr(kt), _ptr(vt), _ptr(k_out), _ptr(v_out),
                                    _ptr(idx_out), _ptr(scores_out), _stream(stream)))
+
+    def exchange(self, y_local, y_recv, stream=None):
+        """Head-group sharding: the NCCL exchange step alone (y_local [b-a, H_l, N] -> y_recv [L_l, nh, N])."""
+        check(lib().pkv_pruner_exchange(self.h, _ptr(y_local), _ptr(y_recv), _stream(stream)))
 
     def run_lse(self, q, kp, lse, kt, vt, k_out, v_out, idx_out=None, scores_out=None, stream=None):
         """Paper regime: the row LSE [L_s, Hq, N] from the proxy's prefill attention

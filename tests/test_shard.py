@@ -111,25 +111,34 @@ def _worker(rank, world, port, name, N, rho, mode, q):
         # this rank's mapper output: target layers [a, b), all heads
         y_local = {t: _yhat(t, g, N) for t in range(p.a, p.b)}
         if mode == P.SHARD_HEAD:
+            # the library's own exchange schedule (pkv_shard_exchange_schedule:
+            # the ops the NCCL exchange issues), executed over gloo
             nh = p.h_hi - p.h_lo
             y_sel = np.zeros((g.target_layers, nh, N), np.float32)
-            reqs, bufs = [], {}
-            for t in range(p.a, p.b):  # sends, one per (target layer, peer)
-                for dst in range(world):
-                    rows = y_local[t][plans[dst].h_lo:plans[dst].h_hi]
-                    if dst == rank:
-                        y_sel[t] = rows
-                    elif rows.size:
-                        reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(rows)), dst, tag=t))
-            for t in range(g.target_layers):  # receives from each layer's producer
-                src = next(r for r in range(world) if plans[r].a <= t < plans[r].b)
-                if src != rank and nh:
-                    bufs[t] = torch.empty(nh, N)
-                    reqs.append(dist.irecv(bufs[t], src, tag=t))
+            flat_local = (np.concatenate([y_local[t] for t in range(p.a, p.b)]).reshape(-1)
+                          if p.b > p.a else np.zeros(0, np.float32))
+            flat_sel = y_sel.reshape(-1)
+            ops = P.shard_exchange_schedule(g, world, rank, N)
+            reqs, bufs, self_sends = [], [], {}
+            for kind, peer, off, cnt, tag in ops.tolist():
+                if kind == 0:
+                    rows = flat_local[off:off + cnt]
+                    if peer == rank:
+                        self_sends[tag] = rows
+                    else:
+                        reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(rows)), peer, tag=tag))
+                else:
+                    if peer == rank:
+                        flat_sel[off:off + cnt] = self_sends.pop(tag)
+                    else:
+                        b = torch.empty(cnt)
+                        reqs.append(dist.irecv(b, peer, tag=tag))
+                        bufs.append((off, cnt, b))
+            assert not self_sends
             for r_ in reqs:
                 r_.wait()
-            for t, b in bufs.items():
-                y_sel[t] = b.numpy()
+            for off, cnt, b in bufs:
+                flat_sel[off:off + cnt] = b.numpy()
             slices = y_sel.reshape(-1, N)
         else:
             slices = np.concatenate([y_local[t] for t in range(p.t_lo, p.t_hi)]).reshape(-1, N)
@@ -147,13 +156,13 @@ def _free_port():
     return port
 
 
-@pytest.mark.parametrize("mode_name", ["head", "layer"])
-@pytest.mark.parametrize("name", ["tiny", "llama"])
-def test_gloo_world2_sharded_select_matches_single_rank(mode_name, name):
+@pytest.mark.parametrize("mode_name,name,world", [("head", "tiny", 2), ("layer", "tiny", 2), ("head", "llama", 2),
+                                                 ("layer", "llama", 2), ("head", "qwen3", 4), ("head", "qwen25", 3)])
+def test_gloo_sharded_select_matches_single_rank(mode_name, name, world):
     import torch.multiprocessing as mp
     import paper_2605_16360_b200 as P
     mode = P.SHARD_HEAD if mode_name == "head" else P.SHARD_LAYER
-    world, N, rho = 2, 512, 0.2
+    N, rho = 512, 0.2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -162,7 +171,7 @@ def test_gloo_world2_sharded_select_matches_single_rank(mode_name, name):
         pr.start()
     res = {}
     for _ in range(world):
-        rank, plan, idx = q.get(timeout=300)
+        rank, plan, idx = q.get(timeout=120)
         res[rank] = (plan, idx)
     for pr in procs:
         pr.join(timeout=60)
@@ -175,3 +184,38 @@ def test_gloo_world2_sharded_select_matches_single_rank(mode_name, name):
     for rank, (plan, idx) in res.items():
         got = idx.reshape(plan.t_hi - plan.t_lo, plan.h_hi - plan.h_lo, k)
         np.testing.assert_array_equal(got, ref[plan.t_lo:plan.t_hi, plan.h_lo:plan.h_hi])
+
+
+@pytest.mark.parametrize("name", sorted(GEOMS))
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_exchange_schedule_matches_across_ranks(name, world):
+    """pkv_shard_exchange_schedule over all ranks: every recv has exactly one
+    send with the same (peer pair, tag, count); the recvs of a rank tile its
+    y_recv [L_l, nh, N] exactly once; each send reads inside y_local."""
+    import paper_2605_16360_b200 as P
+    g = _geom(name)
+    if world > g.target_heads:
+        return
+    N = 100
+    plans = [P.shard_plan(g, world, r, P.SHARD_HEAD) for r in range(world)]
+    ops = [P.shard_exchange_schedule(g, world, r, N) for r in range(world)]
+    sends = {}
+    for r in range(world):
+        p = plans[r]
+        cover = np.zeros(g.target_layers * (p.h_hi - p.h_lo) * N, int)
+        for kind, peer, off, cnt, tag in ops[r].tolist():
+            if kind == 0:
+                assert p.a <= tag < p.b and 0 <= off and off + cnt <= (p.b - p.a) * g.target_heads * N
+                key = (r, peer, tag)
+                assert key not in sends
+                sends[key] = cnt
+            else:
+                cover[off:off + cnt] += 1
+        assert (cover == 1).all()
+    n_recv = 0
+    for r in range(world):
+        for kind, peer, off, cnt, tag in ops[r].tolist():
+            if kind == 1:
+                assert sends.pop((peer, r, tag)) == cnt
+                n_recv += 1
+    assert not sends and n_recv == g.target_layers * sum(1 for p in plans if p.h_hi > p.h_lo)

@@ -112,9 +112,11 @@ def test_pruner_sum_mode_long_context(gpu):
     kp = torch.randn(Ls, Hs, N, dp, device="cuda", generator=gen)
     u = torch.randn(dp, device="cuda", generator=gen)
     u = u / u.norm()
-    kp[:, :, 0] += 6.0 * u  # one dominant sink key per head
-    kp[:, :, 1:N // 50] += 1.5 * u
-    q += 1.5 * u
+    # one dominant sink key per head: q·k_0/√d ≈ 20 > log N, so nearly every
+    # query's softmax puts its mass there and X[0] -> g·N_q
+    kp[:, :, 0] += 20.0 * u
+    kp[:, :, 1:N // 50] += 2.0 * u
+    q += 8.0 * u
     q, kp = q.to(torch.bfloat16), kp.to(torch.bfloat16)
     kt = torch.randn(Ll, Hl, N, dt, device="cuda", generator=gen).to(torch.bfloat16)
     vt = torch.randn(Ll, Hl, N, dt, device="cuda", generator=gen).to(torch.bfloat16)
