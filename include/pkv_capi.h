@@ -87,6 +87,16 @@ pkv_status pkv_topk_select_f64(pkv_ctx ctx, const double* scores_dev, int64_t sl
  * keys, bit-exact for any input without NaN); H2D/D2H inside. */
 pkv_status pkv_topk_mask_host(pkv_ctx ctx, const double* scores_host, int64_t slices, int64_t n, double rho,
                               uint8_t* bits_host, int64_t* k_out);
+/* Replaces topk_indices (pruning.cpp:20-35): the k best of values[0..n) by
+ * the reference order (ties to the lower index), fp64 exact; returned in
+ * ASCENDING index order (the reference leaves them in nth_element order; the
+ * set is identical). PKV_EVALUE "top-k count k out of range for length n". */
+pkv_status pkv_topk_indices_host(pkv_ctx ctx, const double* values_host, int64_t n, int64_t k, int64_t* idx_out);
+/* Replaces topk_overlap_per_slice (pruning.cpp:91-108) on host masks u8
+ * [slices, n] with per-slice count k: |a ∩ b| / k per slice, computed on the
+ * device. */
+pkv_status pkv_topk_overlap_host(pkv_ctx ctx, const uint8_t* mask_a_host, const uint8_t* mask_b_host, int64_t slices,
+                                 int64_t n, int64_t k, double* per_slice_out);
 
 /* Ranking metrics on the device, per slice, fp64:
  * replaces topk_overlap_per_slice (pruning.cpp:91-108: |a ∩ b| / k) and
@@ -239,6 +249,25 @@ pkv_status pkv_mapper_forward_full(pkv_mapper m, const float* x_all_dev, int64_t
  * x fp32 [B, H_s, N] -> y fp32 [B, H_l, N]. */
 pkv_status pkv_mapper_sliding_forward(pkv_mapper m, const float* x_dev, int64_t B, int64_t N, float* y_dev,
                                       void* stream);
+/* Replaces forward_pair, proj/src/mapper.cpp:274-342 (mapper.hpp:118-119),
+ * eval mode: x fp32 [B, H_s, n] -> y fp32 [B, H_l, n], n <= crop_len
+ * (PKV_EVALUE "... long inputs go through sliding_forward" otherwise, as
+ * mapper.cpp:281-282). attn_dev (nullable) receives the StageTrace capture,
+ * the Stage-3 attention fp32 [B, n, H_l, H_syn] (mapper.hpp:111-114; left
+ * untouched when stage_cross is bypassed, where the reference records none). */
+pkv_status pkv_mapper_forward_pair(pkv_mapper m, const float* x_dev, int64_t B, int64_t n, float* y_dev,
+                                   float* attn_dev, void* stream);
+
+/* Host-tensor forms of the three (the reference's own calling convention:
+ * fp64 row-major host buffers in and out; the device computes in the
+ * precision mode the mapper was created with, from the fp32 rounding of x).
+ * Synchronous. attn_host as above (nullable). */
+pkv_status pkv_mapper_forward_pair_host(pkv_mapper m, const double* x_host, int64_t B, int64_t n, double* y_host,
+                                        double* attn_host);
+pkv_status pkv_mapper_sliding_forward_host(pkv_mapper m, const double* x_host, int64_t B, int64_t N,
+                                           double* y_host);
+pkv_status pkv_mapper_forward_full_host(pkv_mapper m, const double* x_all_host, int64_t B, int64_t N,
+                                        double* y_all_host);
 
 /* ------------------------------------------------- whole path (a-1..a-4) -- */
 /* A pruner owns the workspaces for one context shape:

@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -91,6 +92,48 @@ inline int64_t retention_count(double rho, int64_t n) {
     return k;
 }
 
+// The reference's host container (tensor.hpp:42-83): shape + row-major fp64
+// data (its autodiff tape does not cross the boundary).
+struct Tensor {
+    Shape shape;
+    std::vector<double> data;
+    Tensor() = default;
+    Tensor(Shape s, std::vector<double> d) : shape(std::move(s)), data(std::move(d)) {
+        if (static_cast<int64_t>(data.size()) != numel()) throw ShapeError("tensor data does not match its shape");
+    }
+    explicit Tensor(Shape s) : shape(std::move(s)), data(static_cast<size_t>(numel()), 0.0) {}
+    int64_t dim() const { return static_cast<int64_t>(shape.size()); }
+    int64_t size(int64_t i) const { return shape.at(static_cast<size_t>(i)); }
+    int64_t numel() const {
+        int64_t n = 1;
+        for (int64_t e : shape) n *= e;
+        return n;
+    }
+};
+using ScoreTensor = Tensor;  // tensor.hpp:86
+
+inline std::string shape_str(const Shape& s) {
+    std::string o = "[";
+    for (size_t i = 0; i < s.size(); ++i) o += (i ? ", " : "") + std::to_string(s[i]);
+    return o + "]";
+}
+
+// The process-wide context the reference-signature overloads below use
+// (device 0; the reference API has no context argument).
+inline Context& default_context() {
+    static Context c(0);
+    return c;
+}
+
+// pruning.hpp:18 / pruning.cpp:20-35: the k best of values[0..n) (ties to the
+// lower index) on the GPU, fp64 exact. Ascending order (the reference returns
+// nth_element order; same set).
+inline std::vector<int64_t> topk_indices(const double* values, int64_t n, int64_t k) {
+    std::vector<int64_t> idx(static_cast<size_t>(k > 0 ? k : 0));
+    check(pkv_topk_indices_host(default_context().get(), values, n, k, idx.data()));
+    return idx;
+}
+
 // pruning.hpp:22-30
 struct PruneMask {
     Shape shape;
@@ -105,8 +148,8 @@ struct PruneMask {
     }
 };
 
-// pruning.hpp:32 / pruning.cpp:37-56 — scores row-major fp64 (fp32-representable
-// for bit-exact parity), last axis = tokens. Runs the GPU radix select.
+// pruning.hpp:32 / pruning.cpp:37-56 — scores row-major fp64 (ranked exactly:
+// 64-bit order keys), last axis = tokens. Runs the GPU radix select.
 inline PruneMask topk_mask(const Context& ctx, const std::vector<double>& scores, const Shape& shape, double rho) {
     if (shape.empty()) throw ShapeError("topk_mask needs a shaped tensor");
     PruneMask m;
@@ -117,6 +160,32 @@ inline PruneMask topk_mask(const Context& ctx, const std::vector<double>& scores
     check(pkv_topk_mask_host(ctx.get(), scores.data(), static_cast<int64_t>(scores.size()) / n, n, rho,
                              m.bits.data(), &m.k));
     return m;
+}
+
+// pruning.hpp:32 with the reference signature (default context)
+inline PruneMask topk_mask(const ScoreTensor& scores, double rho) {
+    return topk_mask(default_context(), scores.data, scores.shape, rho);
+}
+
+// pruning.hpp:41-42 / pruning.cpp:91-117 (per-slice |a ∩ b| / k on the GPU,
+// then the unweighted slice mean)
+inline std::vector<double> topk_overlap_per_slice(const PruneMask& a, const PruneMask& b) {
+    if (a.shape != b.shape)
+        throw ShapeError("mask shapes differ: " + shape_str(a.shape) + " vs " + shape_str(b.shape));
+    if (a.k != b.k)
+        throw ValueError("topk_overlap needs equal per-slice counts, got " + std::to_string(a.k) + " and " +
+                         std::to_string(b.k));
+    std::vector<double> out(static_cast<size_t>(a.slice_count()));
+    check(pkv_topk_overlap_host(default_context().get(), a.bits.data(), b.bits.data(), a.slice_count(),
+                                a.token_count(), a.k, out.data()));
+    return out;
+}
+
+inline double topk_overlap(const PruneMask& a, const PruneMask& b) {
+    const auto per = topk_overlap_per_slice(a, b);
+    double acc = 0.0;
+    for (double v : per) acc += v;
+    return acc / static_cast<double>(per.size());
 }
 
 // pruning.hpp:48-53, 57 / pruning.cpp:197-215
@@ -212,6 +281,80 @@ private:
     pkv_mapper h_ = nullptr;
     ModelGeometry geom_;
 };
+
+// ---- the reference's mapper entry points on host tensors (mapper.hpp:94-126)
+
+// mapper.hpp:67-100: the parameters (the reference initialisation as the flat
+// fp64 blob, named_parameters + named_buffers order) and, on first use, their
+// device-resident form. Eval only, like sliding_forward / forward_full.
+struct MapperParams {
+    ModelGeometry geometry;
+    MapperConfig config;
+    std::vector<double> blob;
+    uint32_t precision = PKV_MAPPER_FP16X3;
+
+    static MapperParams init(const ModelGeometry& g, const MapperConfig& c, uint64_t seed) {
+        MapperParams p;
+        p.geometry = g;
+        p.config = c;
+        p.blob = mapper_init_params(g, c, seed);
+        return p;
+    }
+    Mapper& device() {
+        if (!dev_) dev_ = std::make_shared<Mapper>(default_context(), geometry, config, blob, precision);
+        return *dev_;
+    }
+
+private:
+    std::shared_ptr<Mapper> dev_;
+};
+
+// mapper.hpp:111-114
+struct StageTrace {
+    Tensor cross_attention;  // [B, N, H_l, H_syn]
+};
+
+// mapper.hpp:118-119 / mapper.cpp:274-342: x [B, H_s, n] -> raw logits
+// [B, H_l, n], n <= crop_len. training = true is the reference's batch-stat
+// BatchNorm path (training only): not on the GPU prune path -> ValueError.
+inline Tensor forward_pair(const Tensor& x, MapperParams& params, bool training, StageTrace* trace = nullptr) {
+    const ModelGeometry& g = params.geometry;
+    if (x.dim() != 3) throw ShapeError("forward_pair input must be [B, H_s, N], got " + shape_str(x.shape));
+    if (x.size(1) != g.proxy_heads)
+        throw ShapeError("input has " + std::to_string(x.size(1)) + " proxy heads, geometry expects " +
+                         std::to_string(g.proxy_heads));
+    if (training) throw ValueError("forward_pair(training=true) is the training path; the GPU mapper is eval-only");
+    const int64_t B = x.size(0), n = x.size(2);
+    const int64_t syn = params.config.synthetic_heads > 0 ? params.config.synthetic_heads : g.proxy_heads;
+    Tensor y({B, g.target_heads, n});
+    const bool want = trace && params.config.stage_cross == StageMode::kActive;
+    std::vector<double> attn(want ? static_cast<size_t>(B * n * g.target_heads * syn) : 0);
+    check(pkv_mapper_forward_pair_host(params.device().get(), x.data.data(), B, n, y.data.data(),
+                                       want ? attn.data() : nullptr));
+    if (want) trace->cross_attention = Tensor({B, n, g.target_heads, syn}, std::move(attn));
+    return y;
+}
+
+// mapper.hpp:123 / mapper.cpp:344-377: [B, H_s, N] -> [B, H_l, N]
+inline Tensor sliding_forward(const Tensor& x, MapperParams& params) {
+    const ModelGeometry& g = params.geometry;
+    if (x.dim() != 3 || x.size(1) != g.proxy_heads)
+        throw ShapeError("sliding_forward input must be [B, H_s, N], got " + shape_str(x.shape));
+    Tensor y({x.size(0), g.target_heads, x.size(2)});
+    check(pkv_mapper_sliding_forward_host(params.device().get(), x.data.data(), x.size(0), x.size(2), y.data.data()));
+    return y;
+}
+
+// mapper.hpp:126 / mapper.cpp:379-398: [B, L_s, H_s, N] -> [B, L_l, H_l, N]
+inline Tensor forward_full(const Tensor& x_all, MapperParams& params) {
+    const ModelGeometry& g = params.geometry;
+    if (x_all.dim() != 4 || x_all.size(1) != g.proxy_layers || x_all.size(2) != g.proxy_heads)
+        throw ShapeError("forward_full input must be [B, L_s, H_s, N], got " + shape_str(x_all.shape));
+    Tensor y({x_all.size(0), g.target_layers, g.target_heads, x_all.size(3)});
+    check(pkv_mapper_forward_full_host(params.device().get(), x_all.data.data(), x_all.size(0), x_all.size(3),
+                                       y.data.data()));
+    return y;
+}
 
 // pruning.cpp:173-186 over DEVICE fp32 rows [slices, n] -> DEVICE fp64 [slices]
 inline void spearman_per_slice(const Context& ctx, const float* a_dev, const float* b_dev, int64_t slices, int64_t n,

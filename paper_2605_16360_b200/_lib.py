@@ -80,6 +80,12 @@ SIGNATURES = {
     "pkv_retention_count": (ctypes.c_int, [_c_dbl, _c_i64, _c_i64p]),
     "pkv_topk_select": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp]),
     "pkv_topk_select_f64": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp]),
+    "pkv_topk_indices_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_vp]),
+    "pkv_topk_overlap_host": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp]),
+    "pkv_mapper_forward_pair": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp]),
+    "pkv_mapper_forward_pair_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_vp, _c_vp]),
+    "pkv_mapper_sliding_forward_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_vp]),
+    "pkv_mapper_forward_full_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_vp]),
     "pkv_topk_mask_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_dbl, _c_vp, _c_i64p]),
     "pkv_topk_overlap": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp]),
     "pkv_captured_mass": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp]),

@@ -189,6 +189,42 @@ pkv_status pkv_topk_mask_host(pkv_ctx ctx, const double* scores_host, int64_t sl
     });
 }
 
+pkv_status pkv_topk_indices_host(pkv_ctx ctx, const double* values_host, int64_t n, int64_t k, int64_t* idx_out) {
+    return guard([&] {
+        require_ctx(ctx);
+        PKV_REQUIRE_VALUE(k >= 1 && k <= n, "top-k count ", k, " out of range for length ", n);  // pruning.cpp:21
+        PKV_REQUIRE_VALUE(n < (int64_t(1) << 31), "token axis too long: ", n);
+        const size_t un = static_cast<size_t>(n), uk = static_cast<size_t>(k);
+        auto* dev = static_cast<uint8_t*>(ctx->scratch_host_io.get(un * 8 + uk * 4));
+        double* d_v = reinterpret_cast<double*>(dev);
+        int32_t* d_idx = reinterpret_cast<int32_t*>(dev + un * 8);
+        PKV_CUDA(cudaMemcpy(d_v, values_host, un * 8, cudaMemcpyHostToDevice));
+        launch_topk_select_f64(d_v, 1, n, k, nullptr, d_idx, nullptr);
+        count_launch(ctx);
+        std::vector<int32_t> h(uk);
+        PKV_CUDA(cudaMemcpy(h.data(), d_idx, uk * 4, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < uk; ++i) idx_out[i] = h[i];
+    });
+}
+
+pkv_status pkv_topk_overlap_host(pkv_ctx ctx, const uint8_t* a_host, const uint8_t* b_host, int64_t slices, int64_t n,
+                                 int64_t k, double* per_slice_out) {
+    return guard([&] {
+        require_ctx(ctx);
+        PKV_REQUIRE_SHAPE(slices > 0 && n > 0, "topk_overlap extents must be positive");
+        const size_t m = static_cast<size_t>(slices * n);
+        auto* dev = static_cast<uint8_t*>(ctx->scratch_host_io.get(2 * m + 8 * static_cast<size_t>(slices) + 16));
+        uint8_t* d_a = dev;
+        uint8_t* d_b = dev + m;
+        double* d_o = reinterpret_cast<double*>(dev + ((2 * m + 15) & ~size_t(15)));
+        PKV_CUDA(cudaMemcpy(d_a, a_host, m, cudaMemcpyHostToDevice));
+        PKV_CUDA(cudaMemcpy(d_b, b_host, m, cudaMemcpyHostToDevice));
+        const pkv_status st = pkv_topk_overlap(ctx, d_a, d_b, slices, n, k, d_o, nullptr);
+        if (st != PKV_OK) throw Error{st, pkv_last_error()};
+        PKV_CUDA(cudaMemcpy(per_slice_out, d_o, 8 * static_cast<size_t>(slices), cudaMemcpyDeviceToHost));
+    });
+}
+
 pkv_status pkv_compact_kv(pkv_ctx ctx, const void* k_in_dev, const void* v_in_dev, const int32_t* idx_asc_dev,
                           int64_t slices, int64_t n, int64_t k, int64_t d, int64_t elem_bytes, void* k_out_dev,
                           void* v_out_dev, void* stream) {

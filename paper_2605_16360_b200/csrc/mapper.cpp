@@ -465,7 +465,7 @@ void Mapper::gemm(const __half* a_h, const __half* a_l, int64_t M, const WeightP
 // x: caller's scores; unit_off[u]: element offset of unit u's [H_s, N] slab
 // (head stride N); out_unit[o]: unit feeding output row block o of y [n_out, H_l, N].
 void Mapper::run(const float* x, const std::vector<int64_t>& unit_off, int64_t N, const std::vector<int>& out_unit,
-                 float* y, cudaStream_t st) {
+                 float* y, cudaStream_t st, float* trace) {
     const int64_t D = cfg.d_time, mid = cfg.conv_mid(), F = cfg.ffn_mult * D, hl = geom.target_heads;
     const int64_t syn = cfg.syn(geom), hs = geom.proxy_heads;
     const auto offs = window_offsets(N, cfg.crop_len, cfg.stride);
@@ -597,7 +597,8 @@ void Mapper::run(const float* x, const std::vector<int64_t>& unit_off, int64_t N
             p.row_scale = rscale;
             gemm(zp_h, zp_l, rows, stage3, stage3_b, EPI_F32, p, st);
             launch_stage3(s3, rows, static_cast<int>(ld3), static_cast<int>(hl), static_cast<int>(syn),
-                          cfg.cross_active, out_b, static_cast<int>(Lw), logitsT + u0 * W * hl * Lw, st);
+                          cfg.cross_active, out_b, static_cast<int>(Lw), logitsT + u0 * W * hl * Lw,
+                          (trace && cfg.cross_active) ? trace + u0 * W * Lw * hl * syn : nullptr, st);
             count_launch(ctx);
         }
     }
@@ -613,6 +614,49 @@ void Mapper::run(const float* x, const std::vector<int64_t>& unit_off, int64_t N
 }  // namespace pkv
 
 using namespace pkv;
+
+namespace {
+
+void run_batch(Mapper& m, const float* x, int64_t B, int64_t N, float* y, cudaStream_t st, float* trace = nullptr) {
+    std::vector<int64_t> unit_off(B);
+    std::vector<int> out_unit(B);
+    for (int64_t b = 0; b < B; ++b) {
+        unit_off[b] = b * m.geom.proxy_heads * N;
+        out_unit[b] = static_cast<int>(b);
+    }
+    m.run(x, unit_off, N, out_unit, y, st, trace);
+}
+
+// mapper.cpp:277-282
+void check_pair_input(const Mapper& m, int64_t B, int64_t n) {
+    PKV_REQUIRE_SHAPE(B > 0 && n > 0, "forward_pair input must be [B, H_s, N] with positive extents");
+    PKV_REQUIRE_VALUE(n <= m.cfg.crop_len, "input length ", n, " exceeds crop_len ", m.cfg.crop_len,
+                      "; long inputs go through sliding_forward");
+}
+
+// Host fp64 in -> device fp32 -> fn -> host fp64 out (synchronous, the
+// mapper's own default-stream scratch).
+template <typename F>
+void host_roundtrip(const double* xh, size_t nx, double* yh, size_t ny, double* ah, size_t na, F&& fn) {
+    std::vector<float> xf(nx);
+    for (size_t i = 0; i < nx; ++i) xf[i] = static_cast<float>(xh[i]);
+    float* d = nullptr;
+    const size_t bytes = (nx + ny + na) * sizeof(float);
+    PKV_CUDA(cudaMalloc(&d, bytes));
+    struct Free {
+        float* p;
+        ~Free() { cudaFree(p); }
+    } guard_free{d};
+    PKV_CUDA(cudaMemcpy(d, xf.data(), nx * sizeof(float), cudaMemcpyHostToDevice));
+    fn(d, d + nx, na ? d + nx + ny : nullptr);
+    PKV_CUDA(cudaStreamSynchronize(nullptr));
+    std::vector<float> yf(ny + na);
+    PKV_CUDA(cudaMemcpy(yf.data(), d + nx, (ny + na) * sizeof(float), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < ny; ++i) yh[i] = yf[i];
+    for (size_t i = 0; i < na; ++i) ah[i] = yf[ny + i];
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -691,18 +735,64 @@ pkv_status pkv_mapper_forward_full(pkv_mapper mh, const float* x_all, int64_t B,
     });
 }
 
+pkv_status pkv_mapper_forward_pair(pkv_mapper mh, const float* x, int64_t B, int64_t n, float* y, float* attn,
+                                   void* stream) {
+    return guard([&] {
+        PKV_REQUIRE_VALUE(mh != nullptr, "null pkv_mapper");
+        Mapper& m = *mh->m;
+        check_pair_input(m, B, n);
+        run_batch(m, x, B, n, y, static_cast<cudaStream_t>(stream), attn);
+    });
+}
+
+pkv_status pkv_mapper_forward_pair_host(pkv_mapper mh, const double* x, int64_t B, int64_t n, double* y,
+                                        double* attn) {
+    return guard([&] {
+        PKV_REQUIRE_VALUE(mh != nullptr, "null pkv_mapper");
+        Mapper& m = *mh->m;
+        check_pair_input(m, B, n);
+        PKV_CUDA(cudaSetDevice(m.ctx->device));
+        const int64_t hl = m.geom.target_heads, syn = m.cfg.syn(m.geom);
+        const size_t na = (attn && m.cfg.cross_active) ? static_cast<size_t>(B * n * hl * syn) : 0;
+        host_roundtrip(x, static_cast<size_t>(B * m.geom.proxy_heads * n), y, static_cast<size_t>(B * hl * n), attn,
+                       na, [&](const float* xd, float* yd, float* ad) { run_batch(m, xd, B, n, yd, nullptr, ad); });
+    });
+}
+
+pkv_status pkv_mapper_sliding_forward_host(pkv_mapper mh, const double* x, int64_t B, int64_t N, double* y) {
+    return guard([&] {
+        PKV_REQUIRE_VALUE(mh != nullptr, "null pkv_mapper");
+        Mapper& m = *mh->m;
+        PKV_REQUIRE_SHAPE(B > 0 && N > 0, "sliding_forward input must be [B, H_s, N]");
+        PKV_CUDA(cudaSetDevice(m.ctx->device));
+        host_roundtrip(x, static_cast<size_t>(B * m.geom.proxy_heads * N), y,
+                       static_cast<size_t>(B * m.geom.target_heads * N), nullptr, 0,
+                       [&](const float* xd, float* yd, float*) { run_batch(m, xd, B, N, yd, nullptr); });
+    });
+}
+
+pkv_status pkv_mapper_forward_full_host(pkv_mapper mh, const double* x, int64_t B, int64_t N, double* y) {
+    return guard([&] {
+        PKV_REQUIRE_VALUE(mh != nullptr, "null pkv_mapper");
+        Mapper& m = *mh->m;
+        PKV_REQUIRE_SHAPE(B > 0 && N > 0, "forward_full input must be [B, L_s, H_s, N] with positive extents");
+        PKV_CUDA(cudaSetDevice(m.ctx->device));
+        const Geometry& g = m.geom;
+        host_roundtrip(x, static_cast<size_t>(B * g.proxy_layers * g.proxy_heads * N), y,
+                       static_cast<size_t>(B * g.target_layers * g.target_heads * N), nullptr, 0,
+                       [&](const float* xd, float* yd, float*) {
+                           PKV_REQUIRE(pkv_mapper_forward_full(mh, xd, B, N, yd, nullptr) == PKV_OK, PKV_ECUDA,
+                                       "forward_full failed");
+                       });
+    });
+}
+
 pkv_status pkv_mapper_sliding_forward(pkv_mapper mh, const float* x, int64_t B, int64_t N, float* y, void* stream) {
     return guard([&] {
         PKV_REQUIRE_VALUE(mh != nullptr, "null pkv_mapper");
         Mapper& m = *mh->m;
         PKV_REQUIRE_SHAPE(B > 0 && N > 0, "sliding_forward input must be [B, H_s, N]");
-        std::vector<int64_t> unit_off(B);
-        std::vector<int> out_unit(B);
-        for (int64_t b = 0; b < B; ++b) {
-            unit_off[b] = b * m.geom.proxy_heads * N;
-            out_unit[b] = static_cast<int>(b);
-        }
-        m.run(x, unit_off, N, out_unit, y, static_cast<cudaStream_t>(stream));
+        run_batch(m, x, B, N, y, static_cast<cudaStream_t>(stream));
     });
 }
 

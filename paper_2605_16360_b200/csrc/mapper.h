@@ -52,8 +52,9 @@ class Mapper {
 public:
     Mapper(pkv_ctx ctx, const Geometry& g, const Config& c, const double* blob, int64_t count, uint32_t precision);
     ~Mapper();
+    // trace (nullable): Stage-3 attention [rows, H_l, syn] of every (unit, window, token) row
     void run(const float* x, const std::vector<int64_t>& unit_off, int64_t N, const std::vector<int>& out_unit,
-             float* y, cudaStream_t st);
+             float* y, cudaStream_t st, float* trace = nullptr);
 
     pkv_ctx ctx;
     Geometry geom;

@@ -272,8 +272,9 @@ __global__ void window_colmean_add_kernel(float* __restrict__ z, int Lw, int D) 
 }
 
 // s3 row = [scores (H_l x syn, already q·k/√dh incl. bias) | v'_s (syn)].
+// attn (nullable, StageTrace, mapper.hpp:111-114): [row, H_l, syn] softmax weights.
 __global__ void stage3_kernel(const float* __restrict__ s3, int64_t rows, int ld, int hl, int syn, int cross_active,
-                              float out_b, int Lw, float* __restrict__ logitsT) {
+                              float out_b, int Lw, float* __restrict__ logitsT, float* __restrict__ attn) {
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= rows) return;
     const float* r = s3 + row * ld;
@@ -292,6 +293,10 @@ __global__ void stage3_kernel(const float* __restrict__ s3, int64_t rows, int ld
                 acc = fmaf(e, vp[s], acc);
             }
             logit = acc / z + out_b;
+            if (attn) {
+                const float iz = 1.0f / z;
+                for (int s = 0; s < syn; ++s) attn[(row * hl + h) * syn + s] = __expf(sc[s] - m) * iz;
+            }
         } else {
             float acc = 0.0f;
             for (int s = 0; s < syn; ++s) acc += vp[s];
@@ -388,9 +393,9 @@ void launch_window_colmean_add(float* z, int64_t nwin, int Lw, int D, cudaStream
 }
 
 void launch_stage3(const float* s3, int64_t rows, int ld, int hl, int syn, bool cross_active, float out_b, int Lw,
-                   float* logitsT, cudaStream_t st) {
+                   float* logitsT, float* attn, cudaStream_t st) {
     stage3_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(s3, rows, ld, hl, syn, cross_active ? 1 : 0, out_b,
-                                                                 Lw, logitsT);
+                                                                 Lw, logitsT, attn);
     check_launch("stage3_kernel");
 }
 

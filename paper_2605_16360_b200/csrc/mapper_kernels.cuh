@@ -27,7 +27,7 @@ void launch_layernorm(const float* z, int64_t rows, int D, const float* g, const
                       cudaStream_t st);
 void launch_window_colmean_add(float* z, int64_t nwin, int Lw, int D, cudaStream_t st);
 void launch_stage3(const float* s3, int64_t rows, int ld, int hl, int syn, bool cross_active, float out_b, int Lw,
-                   float* logitsT, cudaStream_t st);
+                   float* logitsT, float* attn, cudaStream_t st);
 void launch_window_average(const float* logitsT, const int* out_unit, int n_out, int hl, int W, int Lw, int stride,
                            int n_regular, int tail_off, int64_t N, float* y, cudaStream_t st);
 

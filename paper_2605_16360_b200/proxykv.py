@@ -22,7 +22,7 @@ from ._lib import (BadMagicError, ConfigError, CudaError, IoError, NoDeviceError
 
 __all__ = [
     "Context", "PruneMask", "MaskApplication", "ModelGeometry", "MapperConfig", "Mapper", "Pruner",
-    "retention_count", "topk_select", "topk_mask", "apply_mask", "compact_kv", "score", "score_lse",
+    "retention_count", "topk_select", "topk_indices", "topk_mask", "apply_mask", "compact_kv", "score", "score_lse",
     "proxy_prefill_attention", "packed_decode_attention", "paged_decode_attention", "compact_kv_paged", "topk_overlap_device", "captured_mass_device",
     "spearman_device", "slice_metrics_device", "MetricAccumulator", "MetricReport",
     "LossConfig", "LossReport", "loss_total",
@@ -112,6 +112,15 @@ def topk_select(scores, k: int, *, want_mask: bool = True, want_idx: bool = True
     fn = lib().pkv_topk_select_f64 if s.dtype == torch.float64 else lib().pkv_topk_select
     check(fn(ctx.h, _ptr(s), slices, n, int(k), _ptr(mask), _ptr(idx), _stream(stream)))
     return mask, idx
+
+
+def topk_indices(values: np.ndarray, k: int, ctx: Context = None) -> np.ndarray:
+    """pruning.cpp:20-35 on a host fp64 row: the k best (ties to the lower index), ascending."""
+    ctx = ctx or Context.default()
+    v = np.ascontiguousarray(values, np.float64).reshape(-1)
+    out = np.zeros(max(int(k), 0), np.int64)
+    check(lib().pkv_topk_indices_host(ctx.h, v.ctypes.data, v.size, int(k), out.ctypes.data))
+    return out
 
 
 @dataclass
@@ -576,7 +585,50 @@ class Mapper:
         check(lib().pkv_mapper_sliding_forward(self.h, _ptr(x), B, n, _ptr(y), _stream(stream)))
         return y
 
-    forward_pair = sliding_forward
+    def forward_pair(self, x, stream=None, trace: Optional[dict] = None):
+        """forward_pair (mapper.cpp:274-342): x fp32 cuda [B, H_s, n <= crop_len] -> [B, H_l, n]; with
+        `trace` a dict, trace["cross_attention"] = the Stage-3 attention [B, n, H_l, H_syn] (StageTrace)."""
+        torch = _torch()
+        B, hs, n = x.shape
+        x = x.contiguous()
+        y = torch.empty((B, self.geom.target_heads, n), dtype=torch.float32, device=x.device)
+        attn = None
+        if trace is not None and self.cfg.stage_cross == "active":
+            syn = self.cfg.synthetic_heads or self.geom.proxy_heads
+            attn = torch.empty((B, n, self.geom.target_heads, syn), dtype=torch.float32, device=x.device)
+        check(lib().pkv_mapper_forward_pair(self.h, _ptr(x), B, n, _ptr(y), _ptr(attn), _stream(stream)))
+        if trace is not None and attn is not None:
+            trace["cross_attention"] = attn
+        return y
+
+    def forward_pair_host(self, x: np.ndarray, trace: Optional[dict] = None) -> np.ndarray:
+        """The reference calling convention: fp64 host [B, H_s, n] -> fp64 host [B, H_l, n]."""
+        x = np.ascontiguousarray(x, np.float64)
+        B, hs, n = x.shape
+        y = np.zeros((B, self.geom.target_heads, n))
+        attn = None
+        if trace is not None and self.cfg.stage_cross == "active":
+            syn = self.cfg.synthetic_heads or self.geom.proxy_heads
+            attn = np.zeros((B, n, self.geom.target_heads, syn))
+        check(lib().pkv_mapper_forward_pair_host(self.h, x.ctypes.data, B, n, y.ctypes.data,
+                                                 attn.ctypes.data if attn is not None else None))
+        if attn is not None:
+            trace["cross_attention"] = attn
+        return y
+
+    def sliding_forward_host(self, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.float64)
+        B, hs, n = x.shape
+        y = np.zeros((B, self.geom.target_heads, n))
+        check(lib().pkv_mapper_sliding_forward_host(self.h, x.ctypes.data, B, n, y.ctypes.data))
+        return y
+
+    def forward_full_host(self, x_all: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x_all, np.float64)
+        B, ls, hs, n = x.shape
+        y = np.zeros((B, self.geom.target_layers, self.geom.target_heads, n))
+        check(lib().pkv_mapper_forward_full_host(self.h, x.ctypes.data, B, n, y.ctypes.data))
+        return y
 
 
 @dataclass(frozen=True)

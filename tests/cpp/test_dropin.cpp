@@ -3,8 +3,13 @@
 // test_mapper.cpp). Without a GPU only the host logic and the loud NoDeviceError
 // are exercised; with a B200 the GPU select is checked against the reference's
 // known answers.
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <numeric>
+#include <random>
+#include <string>
 #include <vector>
 
 #include "proxykv_b200/proxykv.hpp"
@@ -19,6 +24,28 @@ static int failures = 0;
             ++failures;                                            \
         }                                                          \
     } while (0)
+
+template <typename E, typename F>
+static bool throws_with(F&& f, const std::string& frag) {
+    try {
+        f();
+    } catch (const E& e) {
+        return std::string(e.what()).find(frag) != std::string::npos;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+// test_pruning.cpp:20-32: the stable-sort oracle (value desc, index asc)
+static std::vector<int64_t> sort_oracle(const std::vector<double>& v, int64_t k) {
+    std::vector<int64_t> idx(v.size());
+    std::iota(idx.begin(), idx.end(), 0);
+    std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return v[a] > v[b]; });
+    idx.resize(static_cast<size_t>(k));
+    std::sort(idx.begin(), idx.end());
+    return idx;
+}
 
 template <typename E, typename F>
 static bool throws(F&& f) {
@@ -72,6 +99,82 @@ int main() {
     MaskApplication app = apply_mask(a, 128, 2);
     CHECK((app.retained[0] == std::vector<int64_t>{0, 2}));
     CHECK(app.bytes_saved_per_head == 3 * 128 * 2 * 2);
+
+    // ---- reference signatures (no context argument) ----
+    // topk_indices (pruning.cpp:20-35) on doubles that collide in fp32
+    {
+        std::mt19937_64 rng(7);
+        std::vector<double> v(5000);
+        for (size_t i = 0; i < v.size(); ++i) v[i] = 0.25 + double(rng() % 7) / 8.0 + double(rng() % 1000003) * 1e-13;
+        for (int64_t k : {1, 17, 1000, 4999, 5000}) {
+            auto got = topk_indices(v.data(), static_cast<int64_t>(v.size()), k);
+            CHECK(got == sort_oracle(v, k));
+        }
+        CHECK(throws_with<ValueError>([&] { topk_indices(v.data(), 10, 11); }, "out of range"));
+        ScoreTensor st({2, 2500}, v);
+        PruneMask pm = topk_mask(st, 0.2);
+        CHECK(pm.k == 500);
+        for (int s = 0; s < 2; ++s) {
+            std::vector<double> row(v.begin() + s * 2500, v.begin() + (s + 1) * 2500);
+            const auto want = sort_oracle(row, 500);
+            std::vector<int64_t> got;
+            for (int64_t i = 0; i < 2500; ++i)
+                if (pm.bits[static_cast<size_t>(s * 2500 + i)]) got.push_back(i);
+            CHECK(got == want);
+        }
+        // topk_overlap: self = 1, symmetric, k mismatch (test_pruning.cpp:141-153)
+        PruneMask pm2 = topk_mask(ScoreTensor({2, 2500}, std::vector<double>(v.rbegin(), v.rend())), 0.2);
+        CHECK(topk_overlap(pm, pm) == 1.0);
+        CHECK(topk_overlap(pm, pm2) == topk_overlap(pm2, pm));
+        PruneMask pm3 = topk_mask(st, 0.3);
+        CHECK(throws<ValueError>([&] { topk_overlap(pm, pm3); }));
+    }
+    // mapper: forward_pair / sliding_forward / forward_full on host tensors
+    {
+        ModelGeometry mg;
+        mg.target_layers = 4;
+        mg.target_heads = 8;
+        mg.proxy_layers = 2;
+        mg.proxy_heads = 4;
+        mg.head_dim = 64;
+        MapperConfig mc;
+        mc.encoder_layers = 2;
+        MapperParams mp = MapperParams::init(mg, mc, 3);
+        std::mt19937_64 rng(11);
+        std::uniform_real_distribution<double> u(0.0, 2.0);
+        Tensor x({2, 4, 300});
+        for (double& e : x.data) e = u(rng);
+        StageTrace tr;
+        Tensor y = forward_pair(x, mp, false, &tr);
+        CHECK((y.shape == Shape{2, 8, 300}));
+        CHECK((tr.cross_attention.shape == Shape{2, 300, 8, 4}));
+        // attention rows sum to 1 (test_mapper.cpp:122-137)
+        double worst = 0.0;
+        for (size_t r = 0; r < tr.cross_attention.data.size() / 4; ++r) {
+            double s = 0.0;
+            for (int j = 0; j < 4; ++j) s += tr.cross_attention.data[r * 4 + j];
+            worst = std::max(worst, std::fabs(s - 1.0));
+        }
+        CHECK(worst < 1e-5);
+        // sliding == forward_pair for N <= crop (test_mapper.cpp:226-234)
+        CHECK(sliding_forward(x, mp).data == y.data);
+        // n > crop -> ValueError naming sliding_forward (test_mapper.cpp:90-96)
+        Tensor xl({1, 4, 2049});
+        CHECK(throws_with<ValueError>([&] { forward_pair(xl, mp, false); }, "sliding_forward"));
+        CHECK(throws<ShapeError>([&] { forward_pair(Tensor({1, 3, 10}), mp, false); }));
+        CHECK(throws<ValueError>([&] { forward_pair(x, mp, true); }));
+        // forward_full pairing {1,1,2,2}: shared pairs bit-identical (test_mapper.cpp:268-292)
+        Tensor xa({1, 2, 4, 2500});
+        for (double& e : xa.data) e = u(rng);
+        Tensor ya = forward_full(xa, mp);
+        CHECK((ya.shape == Shape{1, 4, 8, 2500}));
+        const size_t L = 8 * 2500;
+        CHECK(std::equal(ya.data.begin(), ya.data.begin() + L, ya.data.begin() + L));
+        CHECK(std::equal(ya.data.begin() + 2 * L, ya.data.begin() + 3 * L, ya.data.begin() + 3 * L));
+        // forward_full layer 1 == sliding_forward of proxy layer 1
+        Tensor x1({1, 4, 2500}, std::vector<double>(xa.data.begin(), xa.data.begin() + 4 * 2500));
+        CHECK(std::equal(ya.data.begin(), ya.data.begin() + L, sliding_forward(x1, mp).data.begin()));
+    }
     std::printf("[dropin] gpu checks: %s\n", failures ? "FAILED" : "ok");
     return failures ? 1 : 0;
 }
