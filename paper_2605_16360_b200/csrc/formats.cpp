@@ -13,7 +13,9 @@
 // truncation reported with what was being read); corrupt files map onto its
 // IoError taxonomy (common.hpp:33-52): BadMagicError, VersionMismatchError,
 // TruncatedFileError, PayloadLengthError. Host code only (no device).
+#include <cerrno>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <map>
@@ -95,6 +97,7 @@ TraceHeader read_trace_header(Reader& r) {
     PKV_REQUIRE(v == kTraceVersion, PKV_EIO_VERSION, "trace format version ", v, " (reader supports ", kTraceVersion,
                 ")");
     const uint64_t hl = r.u64("header length");
+    r.need(hl, "header");  // before sizing anything from the file's own fields
     std::string text(hl, '\0');
     r.bytes(text.data(), hl, "header");
     TraceHeader h;
@@ -108,7 +111,13 @@ TraceHeader read_trace_header(Reader& r) {
     auto geti = [&](const char* k) {
         auto it = kv.find(k);
         PKV_REQUIRE(it != kv.end(), PKV_EIO, "trace header lacks '", k, "'");
-        return (int64_t)std::stoll(it->second);
+        const char* b = it->second.c_str();
+        char* e = nullptr;
+        errno = 0;
+        const long long v = std::strtoll(b, &e, 10);
+        PKV_REQUIRE(e != b && *e == '\0' && errno == 0, PKV_EIO, "trace header field '", k, "' is not an integer: '",
+                    it->second, "'");
+        return (int64_t)v;
     };
     h.Ls = geti("L_s");
     h.Hs = geti("H_s");
@@ -119,10 +128,30 @@ TraceHeader read_trace_header(Reader& r) {
     h.samples = geti("samples");
     PKV_REQUIRE(kv.count("dtype") && kv["dtype"] == "f32", PKV_EIO, "trace dtype must be f32");
     if (kv.count("meta")) h.meta = kv["meta"];
-    const uint64_t payload = (uint64_t)h.samples * (uint64_t)(h.x_elems() + h.y_elems()) * 4;
-    PKV_REQUIRE(r.size - r.pos == payload, PKV_EIO_LENGTH, "trace payload is ", r.size - r.pos,
-                " bytes, header geometry implies ", payload);
+    for (int64_t e : {h.Ls, h.Hs, h.Ll, h.Hl, h.N, h.B})
+        PKV_REQUIRE(e > 0 && e < (int64_t(1) << 31), PKV_EIO, "trace header geometry extent ", e, " out of range");
+    PKV_REQUIRE(h.samples >= 0, PKV_EIO, "trace header sample count ", h.samples, " is negative");
+    const unsigned __int128 per = (unsigned __int128)(h.x_elems() + h.y_elems()) * 4;
+    const unsigned __int128 want = per * (unsigned __int128)h.samples;
+    PKV_REQUIRE(want == (unsigned __int128)(r.size - r.pos), PKV_EIO_LENGTH, "trace payload is ", r.size - r.pos,
+                " bytes, header geometry implies ", (unsigned long long)(want > ~0ull ? ~0ull : (uint64_t)want));
     return h;
+}
+
+// guard() for the file readers: anything that is not already a pkv::Error
+// (allocation failure on a hostile size field, stream failures) is an
+// IoError, never a CUDA error.
+template <typename F>
+pkv_status guard_io(F&& f) {
+    return guard([&] {
+        try {
+            f();
+        } catch (const Error&) {
+            throw;
+        } catch (const std::exception& e) {
+            throw Error{PKV_EIO, cat("I/O error: ", e.what())};
+        }
+    });
 }
 
 }  // namespace
@@ -164,7 +193,7 @@ pkv_status pkv_trace_write(const char* path, const int64_t* geom6, int64_t sampl
 }
 
 pkv_status pkv_trace_read_header(const char* path, int64_t* geom6_out, int64_t* samples_out) {
-    return guard([&] {
+    return guard_io([&] {
         Reader r(path);
         const TraceHeader h = read_trace_header(r);
         const int64_t g[6] = {h.Ls, h.Hs, h.Ll, h.Hl, h.N, h.B};
@@ -174,7 +203,7 @@ pkv_status pkv_trace_read_header(const char* path, int64_t* geom6_out, int64_t* 
 }
 
 pkv_status pkv_trace_read(const char* path, float* x_out, float* y_out) {
-    return guard([&] {
+    return guard_io([&] {
         Reader r(path);
         const TraceHeader h = read_trace_header(r);
         for (int64_t s = 0; s < h.samples; ++s) {
@@ -217,7 +246,7 @@ pkv_status pkv_checkpoint_write(const char* path, const int64_t* geom5, const in
 
 pkv_status pkv_checkpoint_read(const char* path, int64_t* geom5_out, int64_t* cfg12_out, double* blob_out,
                                int64_t* count_out) {
-    return guard([&] {
+    return guard_io([&] {
         Reader r(path);
         r.magic("PKVC");
         const uint32_t v = r.u32("format version");
@@ -237,6 +266,7 @@ pkv_status pkv_checkpoint_read(const char* path, int64_t* geom5_out, int64_t* cf
         int64_t total = 0;
         for (const auto& [name, n] : layout) {
             const uint32_t len = r.u32("tensor name length");
+            r.need(len, "tensor name");
             std::string nm(len, '\0');
             r.bytes(nm.data(), len, "tensor name");
             const int64_t cnt = (int64_t)r.u64("tensor size"), off = (int64_t)r.u64("tensor offset");

@@ -65,3 +65,44 @@ def test_checkpoint_round_trip_and_layout(tmp_path):
     with pytest.raises(P.PayloadLengthError):
         P.read_checkpoint(p)
     assert os.path.getsize(p) == len(raw) - 8
+
+
+def test_hostile_size_fields_are_io_errors(tmp_path):
+    """size fields are checked against the file length before any
+    buffer is sized from them; malformed header fields / geometry are IoError
+    (never a CUDA error or a crash)."""
+    import struct
+    import paper_2605_16360_b200 as P
+    bad = str(tmp_path / "bad.pkvt")
+    # header length 2^60 in a 40-byte file
+    open(bad, "wb").write(b"PKVT" + struct.pack("<IQ", 1, 1 << 60) + b"L_s=1\n" * 4)
+    with pytest.raises(P.TruncatedFileError, match="header"):
+        P.read_trace(bad)
+
+    def hdr(text):
+        t = text.encode()
+        open(bad, "wb").write(b"PKVT" + struct.pack("<IQ", 1, len(t)) + t)
+
+    hdr("L_s=abc\nH_s=1\nL_l=1\nH_l=1\nN=4\nB=1\ndtype=f32\nsamples=0\n")
+    with pytest.raises(P.IoError, match="not an integer"):
+        P.read_trace(bad)
+    hdr("L_s=-2\nH_s=1\nL_l=1\nH_l=1\nN=4\nB=1\ndtype=f32\nsamples=0\n")
+    with pytest.raises(P.IoError, match="out of range"):
+        P.read_trace(bad)
+    hdr("L_s=1\nH_s=1\nL_l=1\nH_l=1\nN=4\nB=1\ndtype=f32\nsamples=-1\n")
+    with pytest.raises(P.IoError, match="negative"):
+        P.read_trace(bad)
+    hdr("L_s=2000000000\nH_s=2000000000\nL_l=1\nH_l=1\nN=2000000000\nB=1\ndtype=f32\nsamples=1000\n")
+    with pytest.raises(P.PayloadLengthError):
+        P.read_trace(bad)
+    # checkpoint: a tensor-name length far past the end of the file
+    g = P.ModelGeometry(4, 8, 2, 4, 64)
+    c = P.MapperConfig(encoder_layers=1)
+    ck = str(tmp_path / "m.pkvc")
+    P.write_checkpoint(ck, g, c, P.mapper_init_params(g, c, 1))
+    raw = bytearray(open(ck, "rb").read())
+    off = 4 + 4 + 17 * 8 + 8  # magic, version, geometry, config, tensor count
+    raw[off:off + 4] = struct.pack("<I", 0xFFFFFFF0)
+    open(ck, "wb").write(bytes(raw))
+    with pytest.raises(P.TruncatedFileError, match="tensor name"):
+        P.read_checkpoint(ck)
