@@ -2,8 +2,9 @@
 Llama-3.1-8B target shapes (32 layers x 8 KV heads, head_dim 128, bf16): the
 select + compaction regime, HBM-bound. Per point: select (radix Top-K ->
 ascending indices) and compaction (packed K/V gather) timed with CUDA events
-on the launching stream (5 iterations after 3 warm-ups; inputs > L2 except
-the scores at 8k-16k, which the select reads once), algorithmic bytes per
+on the launching stream through the C ABI with preallocated outputs (20 / 10
+back-to-back launches queued behind a spin kernel, after 3 warm-ups; inputs >
+L2 except the scores at 8k-16k, which the select reads once), algorithmic bytes per
 SURVEY.md §8(d), fraction of MEASURED_PEAKS.json HBM bandwidth.
 
     python tools/bench_sweep.py [--out profiles/r01_sweep.json]
@@ -39,14 +40,18 @@ for N in (8192, 16384, 32768, 65536, 131072):
         K = P.retention_count(rho, N)
         ko = torch.empty(S, K, dt, dtype=torch.bfloat16, device="cuda")
         vo = torch.empty_like(ko)
-        sel = lambda: P.topk_select(scores, K, want_mask=False, ctx=ctx, stream=st)
-        _, idx = sel()
-        cmp = lambda: P.compact_kv(kt, vt, idx, ctx=ctx, stream=st, out=(ko, vo))
+        idx = torch.empty(S, K, dtype=torch.int32, device="cuda")
+        L = P.lib()
+        sel = lambda: P.check(L.pkv_topk_select(ctx.h, scores.data_ptr(), S, N, K, None, idx.data_ptr(),
+                                                st.cuda_stream))
+        sel()
+        cmp = lambda: P.check(L.pkv_compact_kv(ctx.h, kt.data_ptr(), vt.data_ptr(), idx.data_ptr(), S, N, K, dt, 2,
+                                               ko.data_ptr(), vo.data_ptr(), st.cuda_stream))
         for _ in range(3):
             sel()
             cmp()
-        t_sel = bench.time_loop(sel, 5, st)
-        t_cmp = bench.time_loop(cmp, 5, st)
+        t_sel = bench.time_loop(sel, 20, st)
+        t_cmp = bench.time_loop(cmp, 10, st)
         c = dict(Ll=Ll, Hl=Hl, N=N, rho=rho, dt=dt)
         b_sel, b_cmp = bench.bytes_select(c), bench.bytes_compact(c)
         r = dict(N=N, rho=rho, K=K, select_ms=t_sel, compact_ms=t_cmp,
