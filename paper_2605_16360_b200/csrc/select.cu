@@ -406,6 +406,7 @@ __global__ void __launch_bounds__(kT, 1024 / kT)
 //            lowest indices across the whole cluster, pruning.cpp:24-31).
 constexpr int kMaxCluster = 8;
 constexpr int kClusterChunk = 16384;  // target elements per CTA
+constexpr bool kAggregate = true;
 
 __device__ __forceinline__ uint32_t ld_dsmem(uint32_t addr) {
     uint32_t v;
@@ -537,7 +538,15 @@ __device__ __forceinline__ void cluster_pass(ClusterSmem& S, const uint32_t (&ke
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const bool ok = ((vm[t] >> j) & 1u) && (key[t][j] & pmask) == prefix;
-            atomicAdd(&S.hist[ok ? (key[t][j] >> shift) & dmask : trash], 1u);
+            const uint32_t bin = ok ? (key[t][j] >> shift) & dmask : trash;
+            if (kAggregate) {
+                // score rows concentrate in a few exponent buckets: one atomic
+                // per distinct bin per warp instead of one per lane
+                const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+                if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&S.hist[bin], (uint32_t)__popc(peers));
+            } else {
+                atomicAdd(&S.hist[bin], 1u);
+            }
         }
     }
     csync<kT>(C);
@@ -596,7 +605,7 @@ template <int kT>
 __global__ void __launch_bounds__(kT, 1024 / kT)
     topk_select_cluster_kernel(const float* __restrict__ scores, int64_t n, int64_t k, int chunk, int cap,
                                uint8_t* __restrict__ mask, int32_t* __restrict__ idx, int C, bool aligned16,
-                               bool mask8) {
+                               bool mask8, int probe) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     ClusterSmem& S = *reinterpret_cast<ClusterSmem*>(smem_raw);
     const int tid = threadIdx.x;
@@ -631,9 +640,15 @@ __global__ void __launch_bounds__(kT, 1024 / kT)
         }
     }
 
+    // timing probe (PKV_SELECT_PROBE): stop after a phase (all CTAs alike)
+    if (probe == 1) {
+        if (key[0][0] == 0xFFFFFFFFu && key[3][7] == 1u) S.res[0] = 1;  // keep the loads
+        return;
+    }
     // ---- pass 0: the k-th key's 12-bit bucket
     uint32_t kr = (uint32_t)k, b0;
     cluster_pass<kT>(S, key, vm, ntiles, 0u, 0u, 20, 12, kr, b0, C, rank);
+    if (probe == 2) return;
 
     // ---- candidates (keys in bucket b0) -> the leader's list
     uint32_t cm[4], ccount = 0;
@@ -693,6 +708,7 @@ __global__ void __launch_bounds__(kT, 1024 / kT)
         ties = kr;
     }
 
+    if (probe == 3) return;
     // ---- output: (greater, equal) bits per tile, slice-global positions
     // (the bits are recomputed in the write loop: fewer live registers)
     auto gt_eq = [&](int t, uint32_t& g, uint32_t& e) {
@@ -777,12 +793,12 @@ __global__ void __launch_bounds__(kT, 1024 / kT)
 template <int kT>
 void launch_cluster(const float* scores, int64_t slices, int64_t n, int64_t k, int C, int chunk, uint8_t* mask,
                     int32_t* idx, bool a16, bool m8, cudaStream_t st) {
-    const int cap = (int)std::min<int64_t>(16384, std::max<int64_t>(2048, n / 8));
+    const int cap = 4096;  // candidate keys (16 KB): keeps 2+ CTAs per SM
     const size_t smem = sizeof(ClusterSmem) + (size_t)cap * 4;
     auto kern = topk_select_cluster_kernel<kT>;
     static std::atomic<uint64_t> once{0};
     if (first_on_device(once))
-        PKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 20 * 1024 + 16384 * 4));
+        PKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(slices * C));
     cfg.blockDim = dim3(kT);
@@ -795,7 +811,8 @@ void launch_cluster(const float* scores, int64_t slices, int64_t n, int64_t k, i
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    PKV_CUDA(cudaLaunchKernelEx(&cfg, kern, scores, n, k, chunk, cap, mask, idx, C, a16, m8));
+    static const int probe = getenv("PKV_SELECT_PROBE") ? atoi(getenv("PKV_SELECT_PROBE")) : 0;
+    PKV_CUDA(cudaLaunchKernelEx(&cfg, kern, scores, n, k, chunk, cap, mask, idx, C, a16, m8, probe));
 }
 
 }  // namespace
@@ -814,7 +831,8 @@ void launch_topk_select(const float* scores, int64_t slices, int64_t n, int64_t 
     static const int min_kt = getenv("PKV_SELECT_MIN_THREADS") ? atoi(getenv("PKV_SELECT_MIN_THREADS")) : 512;
     static const bool legacy = getenv("PKV_SELECT_LEGACY") != nullptr;  // A/B switch: one CTA per slice
     if (!legacy && n <= (int64_t)kMaxCluster * 32768) {
-        const int C = (int)std::min<int64_t>(kMaxCluster, std::max<int64_t>(1, (n + kClusterChunk - 1) / kClusterChunk));
+        int C = 1;  // power of two (the 4096 pass-0 bins split evenly)
+        while (C < kMaxCluster && (int64_t)C * kClusterChunk < n) C *= 2;
         const int chunk = (int)((((n + C - 1) / C) + 7) / 8 * 8);
         const bool a16c = a16 && (n & 3) == 0;
         const bool m8c = m8 && (n & 7) == 0;

@@ -58,6 +58,29 @@ def test_fullsize_lse_sampled_queries(run):
         assert np.abs(got - want[0, 0]).max() < 2e-4
 
 
+def test_fullsize_x_sampled_keys_fp64_all_queries(run):
+    """llama32k pooled X (max over the 4 query heads x 32768 queries of each KV
+    head) at sampled keys vs a float64 evaluation over ALL queries (with the
+    GPU's LSE, itself checked above against the fp64 restatement): rel 1e-3 of
+    the slab's max; 3 (layer, KV head) slabs x 32 keys."""
+    import torch
+    c = run["c"]
+    g, d, N = c["Hq"] // c["Hs"], c["dp"], c["N"]
+    q, kp, x, lse = run["q"], run["kp"], run["x"], run["lse"]
+    rs = np.random.RandomState(3)
+    for l, kh in [(0, 0), (8, 3), (15, 7)]:
+        qf = q[l, kh * g:(kh + 1) * g].double()
+        ks = torch.from_numpy(np.sort(rs.choice(N, 32, replace=False))).cuda()
+        kf = kp[l, kh, ks].double()
+        s = torch.einsum("gnd,kd->gnk", qf, kf) / d ** 0.5 - lse[l, kh * g:(kh + 1) * g].double()[..., None]
+        xw = torch.exp(s.amax(dim=(0, 1))).cpu().numpy()
+        xg = x[l, kh, ks].double().cpu().numpy()
+        scale = x[l, kh].max().item()
+        err = np.abs(xg - xw).max() / scale
+        print(f"llama32k X (layer {l}, kv head {kh}) sampled-key rel err {err:.2e}")
+        assert err <= 1e-3
+
+
 def test_fullsize_mapper_and_topk_overlap(run):
     c = run["c"]
     N, K = c["N"], run["K"]
