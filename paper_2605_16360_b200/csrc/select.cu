@@ -406,7 +406,9 @@ __global__ void __launch_bounds__(kT, 1024 / kT)
 //            lowest indices across the whole cluster, pruning.cpp:24-31).
 constexpr int kMaxCluster = 8;
 constexpr int kClusterChunk = 16384;  // target elements per CTA
-constexpr bool kAggregate = true;
+constexpr bool kAggregate = false;
+constexpr int kMaxSamples = 4096;
+constexpr int kCandCap = 8192;
 
 __device__ __forceinline__ uint32_t ld_dsmem(uint32_t addr) {
     uint32_t v;
@@ -427,6 +429,7 @@ struct ClusterSmem {
     uint32_t warp_sums[32];
     uint4 warp_sums4[32];
     uint32_t s_digit, s_above;
+    uint32_t samp[kMaxSamples];  // leader: the row sample, sorted descending
     uint32_t cand[1];  // [cap] candidate keys (leader's copy is used)
 };
 
@@ -605,7 +608,7 @@ template <int kT>
 __global__ void __launch_bounds__(kT, 1024 / kT)
     topk_select_cluster_kernel(const float* __restrict__ scores, int64_t n, int64_t k, int chunk, int cap,
                                uint8_t* __restrict__ mask, int32_t* __restrict__ idx, int C, bool aligned16,
-                               bool mask8, int probe) {
+                               bool mask8, int probe, int ns) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     ClusterSmem& S = *reinterpret_cast<ClusterSmem*>(smem_raw);
     const int tid = threadIdx.x;
@@ -645,10 +648,116 @@ __global__ void __launch_bounds__(kT, 1024 / kT)
         if (key[0][0] == 0xFFFFFFFFu && key[3][7] == 1u) S.res[0] = 1;  // keep the loads
         return;
     }
+    uint32_t kth = 0, ties = 0;
+    bool done = false;
+    if (ns > 0) {
+        // ---- sample bracket: NS keys sampled evenly from the whole row (the
+        // slice is L2-resident now), sorted by the leader; [lo, hi] brackets the
+        // k-th key's sample rank by +-3.5 sigma (binomial), so typically a few
+        // % of the row falls inside. Exactness never depends on the sample:
+        // a miss just takes the radix path below.
+        const int spc = ns / C;
+        const int64_t gstride = n / ns;
+        const float* __restrict__ row = scores + slice * n;
+        for (int i = tid; i < spc; i += kT) {
+            const uint32_t kk = order_key(__ldg(row + ((int64_t)rank * spc + i) * gstride));
+            if (C > 1) st_dsmem(peer(&S.samp[rank * spc + i], 0), kk);
+            else S.samp[i] = kk;
+        }
+        csync<kT>(C);
+        if (rank == 0) {
+            for (int size = 2; size <= ns; size <<= 1) {
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (int i = tid; i < ns / 2; i += kT) {
+                        const int a = 2 * i - (i & (stride - 1)), b = a + stride;
+                        const bool desc = (a & size) == 0;
+                        const uint32_t x = S.samp[a], y = S.samp[b];
+                        if ((x < y) == desc) {
+                            S.samp[a] = y;
+                            S.samp[b] = x;
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            if (tid == 0) {
+                const double pr = (double)k / (double)n;
+                const int r = (int)(pr * ns);
+                const int m = (int)(3.5 * sqrt((double)ns * pr * (1.0 - pr))) + 4;
+                const uint32_t hi = r - m >= 0 ? S.samp[r - m] : 0xFFFFFFFFu;
+                const uint32_t lo = r + m < ns ? S.samp[r + m] : 0u;
+                for (int q = 0; q < C; ++q) {
+                    st_dsmem(peer(&S.res[0], (uint32_t)q), lo);
+                    st_dsmem(peer(&S.res[1], (uint32_t)q), hi);
+                }
+            }
+        }
+        csync<kT>(C);
+        const uint32_t lo = S.res[0], hi = S.res[1];
+        // ---- band pass: count above hi, candidates in [lo, hi]
+        uint32_t cm[4], gc = 0, cc = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            cm[t] = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t in = (vm[t] >> j) & 1u, kk = key[t][j];
+                gc += in & (uint32_t)(kk > hi);
+                cm[t] |= (in & (uint32_t)(kk >= lo) & (uint32_t)(kk <= hi)) << j;
+            }
+            cc += __popc(cm[t]);
+        }
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan<kT>(gc | (cc << 16), S.warp_sums, tot);
+        if (tid == 0)
+            for (int q = 0; q < C; ++q) {
+                st_dsmem(peer(&S.gtot[rank], (uint32_t)q), tot & 0xFFFFu);
+                st_dsmem(peer(&S.ctot[rank], (uint32_t)q), tot >> 16);
+            }
+        csync<kT>(C);
+        uint32_t G = 0, Call = 0, before = 0;
+        for (int q = 0; q < C; ++q) {
+            G += S.gtot[q];
+            Call += S.ctot[q];
+            if ((uint32_t)q < rank) before += S.ctot[q];
+        }
+        if (probe == 2) return;
+        if (G < (uint32_t)k && (uint32_t)k <= G + Call && Call <= (uint32_t)cap) {  // cluster-uniform
+            uint32_t pos = before + (ex >> 16);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                if (!cm[t]) continue;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if ((cm[t] >> j) & 1u) {
+                        if (C > 1) st_dsmem(peer(&S.cand[pos], 0), key[t][j]);
+                        else S.cand[pos] = key[t][j];
+                        ++pos;
+                    }
+                }
+            }
+            csync<kT>(C);
+            if (rank == 0) {
+                uint32_t kr = (uint32_t)k - G, d0, d1, d2;
+                list_pass<kT>(S, (int)Call, 0u, 0u, 20, 12, kr, d0);
+                list_pass<kT>(S, (int)Call, d0 << 20, 0xFFF00000u, 8, 12, kr, d1);
+                list_pass<kT>(S, (int)Call, (d0 << 20) | (d1 << 8), 0xFFFFFF00u, 0, 8, kr, d2);
+                if (tid == 0)
+                    for (int q = 0; q < C; ++q) {
+                        st_dsmem(peer(&S.res[2], (uint32_t)q), (d0 << 20) | (d1 << 8) | d2);
+                        st_dsmem(peer(&S.res[3], (uint32_t)q), kr);
+                    }
+            }
+            csync<kT>(C);
+            kth = S.res[2];
+            ties = S.res[3];
+            done = true;
+        }
+    }
+    if (!done) {
     // ---- pass 0: the k-th key's 12-bit bucket
     uint32_t kr = (uint32_t)k, b0;
     cluster_pass<kT>(S, key, vm, ntiles, 0u, 0u, 20, 12, kr, b0, C, rank);
-    if (probe == 2) return;
 
     // ---- candidates (keys in bucket b0) -> the leader's list
     uint32_t cm[4], ccount = 0;
@@ -669,7 +778,6 @@ __global__ void __launch_bounds__(kT, 1024 / kT)
         all += S.ctot[q];
         if ((uint32_t)q < rank) before += S.ctot[q];
     }
-    uint32_t kth, ties;
     if (all <= (uint32_t)cap) {
         uint32_t pos = before + cex;
 #pragma unroll
@@ -707,6 +815,7 @@ __global__ void __launch_bounds__(kT, 1024 / kT)
         kth = p0 | (d1 << 8) | d2;
         ties = kr;
     }
+    }  // radix path
 
     if (probe == 3) return;
     // ---- output: (greater, equal) bits per tile, slice-global positions
@@ -793,7 +902,8 @@ __global__ void __launch_bounds__(kT, 1024 / kT)
 template <int kT>
 void launch_cluster(const float* scores, int64_t slices, int64_t n, int64_t k, int C, int chunk, uint8_t* mask,
                     int32_t* idx, bool a16, bool m8, cudaStream_t st) {
-    const int cap = 4096;  // candidate keys (16 KB): keeps 2+ CTAs per SM
+    const int cap = kCandCap;  // candidate keys (32 KB)
+    const int ns = n >= 65536 ? 4096 : (n >= 4096 ? 2048 : 0);  // sample size (0: radix path only)
     const size_t smem = sizeof(ClusterSmem) + (size_t)cap * 4;
     auto kern = topk_select_cluster_kernel<kT>;
     static std::atomic<uint64_t> once{0};
@@ -812,7 +922,7 @@ void launch_cluster(const float* scores, int64_t slices, int64_t n, int64_t k, i
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     static const int probe = getenv("PKV_SELECT_PROBE") ? atoi(getenv("PKV_SELECT_PROBE")) : 0;
-    PKV_CUDA(cudaLaunchKernelEx(&cfg, kern, scores, n, k, chunk, cap, mask, idx, C, a16, m8, probe));
+    PKV_CUDA(cudaLaunchKernelEx(&cfg, kern, scores, n, k, chunk, cap, mask, idx, C, a16, m8, probe, ns));
 }
 
 }  // namespace
