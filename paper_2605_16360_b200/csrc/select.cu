@@ -659,33 +659,37 @@ __global__ void __launch_bounds__(kT, 1024 / kT)
         const int spc = ns / C;
         const int64_t gstride = n / ns;
         const float* __restrict__ row = scores + slice * n;
+        if (rank == 0)
+            for (int j = tid; j < 4096; j += kT) S.hist[j] = 0;
+        if (C == 1) __syncthreads();
+        else csync<kT>(C);  // the leader's histogram is zeroed before anyone adds
+        const uint32_t hist0 = sm100::smem_u32(&S.hist[0]);
+        const uint32_t hist_leader = C > 1 ? sm100::mapa_shared(hist0, 0) : hist0;
+#pragma unroll 4
         for (int i = tid; i < spc; i += kT) {
             const uint32_t kk = order_key(__ldg(row + ((int64_t)rank * spc + i) * gstride));
-            if (C > 1) st_dsmem(peer(&S.samp[rank * spc + i], 0), kk);
-            else S.samp[i] = kk;
+            const uint32_t addr = hist_leader + ((kk >> 20) << 2);
+            if (C > 1) asm volatile("red.shared::cluster.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+            else atomicAdd(&S.hist[kk >> 20], 1u);
         }
         csync<kT>(C);
         if (rank == 0) {
-            for (int size = 2; size <= ns; size <<= 1) {
-                for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                    for (int i = tid; i < ns / 2; i += kT) {
-                        const int a = 2 * i - (i & (stride - 1)), b = a + stride;
-                        const bool desc = (a & size) == 0;
-                        const uint32_t x = S.samp[a], y = S.samp[b];
-                        if ((x < y) == desc) {
-                            S.samp[a] = y;
-                            S.samp[b] = x;
-                        }
-                    }
-                    __syncthreads();
-                }
-            }
+            // the 12-bit buckets of the sample ranks r - m and r + m bound the
+            // band (bucket granularity: concentrated rows give narrow bands)
+            const double pr = (double)k / (double)n;
+            const int r = (int)(pr * ns);
+            const int m = (int)(3.5 * sqrt((double)ns * pr * (1.0 - pr))) + 4;
+            uint32_t P, dh = 0, ah = 0, dl = 0, al = 0;
+            bool fh, fl;
+            const bool has_hi = r - m >= 1, has_lo = r + m <= ns;
+            scan_bins<kT>(S, 4096, 0, 4096, 1, has_hi ? (uint32_t)(r - m) : 0u, P, fh, dh, ah);
+            if (fh) S.s_digit = dh;
+            scan_bins<kT>(S, 4096, 0, 4096, 1, has_lo ? (uint32_t)(r + m) : 0u, P, fl, dl, al);
+            if (fl) S.s_above = dl;
+            __syncthreads();
             if (tid == 0) {
-                const double pr = (double)k / (double)n;
-                const int r = (int)(pr * ns);
-                const int m = (int)(3.5 * sqrt((double)ns * pr * (1.0 - pr))) + 4;
-                const uint32_t hi = r - m >= 0 ? S.samp[r - m] : 0xFFFFFFFFu;
-                const uint32_t lo = r + m < ns ? S.samp[r + m] : 0u;
+                const uint32_t hi = has_hi ? ((S.s_digit + 1) << 20) - 1u : 0xFFFFFFFFu;
+                const uint32_t lo = has_lo ? S.s_above << 20 : 0u;
                 for (int q = 0; q < C; ++q) {
                     st_dsmem(peer(&S.res[0], (uint32_t)q), lo);
                     st_dsmem(peer(&S.res[1], (uint32_t)q), hi);
