@@ -1,11 +1,12 @@
-"""The cluster Top-K select (select.cu topk_select_cluster_kernel: one CTA
-cluster of C = ceil(n / 16384) <= 8 CTAs per slice, DSMEM histogram merge,
-leader candidate list, register fallback for heavily tied rows) bit-exact
-against the oracle restatement of pruning.cpp:20-56 + 197-215 (mask bytes and
-ascending indices) at every cluster size and chunk boundary, on random,
-tie-heavy (test_pruning.cpp:84-98's floor(8u)/8), all-equal, signed-zero and
-single-bucket rows (every key in the k-th key's 12-bit bucket: the candidate
-list overflows and the register passes run)."""
+"""Top-K select (select.cu: register-cached one-CTA-per-slice radix select
+up to 32768 keys, the L2-re-reading generic kernel beyond) bit-exact against
+the oracle restatement of pruning.cpp:20-56 + 197-215 (mask bytes and
+ascending indices) at every kernel boundary (256 / 512 / 1024 threads, 8
+items x 4 tiles per thread, > 32768 generic) and odd sizes, on random,
+tie-heavy (test_pruning.cpp:84-98's floor(8u)/8), all-equal, signed-zero,
+single-bucket (every key in one 12-bit digit bucket) and mapper-logit rows.
+(Written for the round-2 cluster-select experiment, see
+profiles/r02_select_cluster_experiment.txt; kept as coverage of the default.)"""
 import numpy as np
 import pytest
 
