@@ -205,6 +205,15 @@ def max_over_ranks(v, world, dev):
     return t.item()
 
 
+def gather_obj(world, obj):
+    if world == 1:
+        return [obj]
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, obj)
+    return out
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -321,10 +330,7 @@ def run_ours(args, c, rank, world, local_rank):
     per_rank = {"rank": rank, "ms": ms_rank, **work,
                 "score_map_TFLOP/s": (work["score_flop"] + work["map_flop"]) / (ms_rank * 1e-3) / 1e12}
     if world > 1:
-        import torch.distributed as dist
-        allr = [None] * world
-        dist.all_gather_object(allr, per_rank)
-        result["per_rank"] = allr
+        result["per_rank"] = gather_obj(world, per_rank)
     if rank == 0 and world == 1:
         result["stages"] = stage_breakdown(P, ctx, arm, c, stream, args)
     if not args.no_e2e:
@@ -333,7 +339,7 @@ def run_ours(args, c, rank, world, local_rank):
             result["e2e"] = e
     del arm
     torch.cuda.empty_cache()
-    if world > 1 and not args.no_extras:
+    if (world > 1 and not args.no_extras) or args.extras:
         result["weak_scaling"] = weak_scaling(P, ctx, c, dev, world, rank, args, stream)
         result["sharded_configs"] = sharded_configs(P, ctx, dev, world, rank, args, stream)
     if world > 1:
@@ -367,12 +373,9 @@ def sharded_configs(P, ctx, dev, world, rank, args, stream):
         rec = {"shard": mode, "N": cc["N"], "ms_per_context": ms, "tokens_per_s": cc["N"] / (ms * 1e-3),
                "desc": cc["desc"]}
         work = rank_work(cc, arm.plan)
-        allr = [None] * world
-        import torch.distributed as dist
-        dist.all_gather_object(allr, {"rank": rank, "ms": ms_rank, **work,
-                                      "score_map_TFLOP/s": (work["score_flop"] + work["map_flop"]) /
-                                                           (ms_rank * 1e-3) / 1e12})
-        rec["per_rank"] = allr
+        rec["per_rank"] = gather_obj(world, {"rank": rank, "ms": ms_rank, **work,
+                                             "score_map_TFLOP/s": (work["score_flop"] + work["map_flop"]) /
+                                                                  (ms_rank * 1e-3) / 1e12})
         if mode == "head":
             pl = arm.plan
             y_local = torch.zeros(max(pl.b - pl.a, 1), cc["Hl"], cc["N"], device=dev)
@@ -598,6 +601,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="N > 1: skip weak_scaling and sharded_configs")
+    ap.add_argument("--extras", action="store_true", help="run weak_scaling and sharded_configs even at N = 1 "
+                                                          "(exercises the sharded code paths on one GPU)")
     ap.add_argument("--shard", choices=["auto", "none", "layer", "head"], default="auto",
                     help="auto: none at N = 1, layer at N > 1 (strong scaling of one context); none: weak scaling "
                          "(one independent context per GPU); head: head-group sharding with the NCCL exchange")

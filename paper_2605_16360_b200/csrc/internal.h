@@ -4,6 +4,7 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <atomic>
@@ -96,6 +97,15 @@ inline bool first_on_device(std::atomic<uint64_t>& done) {
     return (done.fetch_or(bit) & bit) == 0;
 }
 inline void count_launch(pkv_ctx ctx, int n = 1) { ctx->launches += n; }
+
+// NVTX range for one stage of the path (per-stage ranges for
+// nsys / ncu --nvtx). Header-only NVTX v3: a no-op unless a tool injects.
+struct StageRange {
+    explicit StageRange(const char* name) { nvtxRangePushA(name); }
+    ~StageRange() { nvtxRangePop(); }
+    StageRange(const StageRange&) = delete;
+    StageRange& operator=(const StageRange&) = delete;
+};
 void check_launch(const char* what);
 
 // ---------------------------------------------------------- kernel entries

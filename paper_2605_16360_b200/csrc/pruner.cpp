@@ -174,6 +174,8 @@ void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, con
         const auto* kpp = static_cast<const uint8_t*>(kp) + k_off;
         auto* lam = static_cast<__nv_bfloat16*>(p->lam.get(static_cast<size_t>(s.L * s.Hq * s.Nq) * 16));
         auto* x = static_cast<float*>(p->x.get(static_cast<size_t>(s.L * s.Hkv * s.Nk) * 4));
+        {
+        StageRange r_score("pkv.score");
         if (lse_in) {  // LSE from the proxy's prefill attention: the pooled pass only
             launch_lam_from_lse(lse_in + static_cast<size_t>(pl.p_lo * p->Hq * p->N), s.L * s.Hq * s.Nq, s.d, lam,
                                 ps);
@@ -198,6 +200,7 @@ void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, con
                 count_launch(p->ctx, 2);
             }
         }
+        }  // pkv.score
         // (2)-(4) per target-layer group with the outputs leaving for the host
         if (arr && arr->k_out_h && pl.mode != PKV_SHARD_HEAD && ts == ps && slices > 0 &&
             n_map * p->Hl == slices) {
@@ -205,10 +208,14 @@ void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, con
             return;
         }
         // (2) mapper: Ŷ for target layers [a, b), all heads
+        StageRange r_map("pkv.map");
         p->mapper->run(x, p->unit_off, p->N, p->out_unit, y_map, ps);
     }
     // (2b) head-group sharding: every mapped row to the owner of its head
-    if (pl.mode == PKV_SHARD_HEAD) exchange_scores(p->comm, pl, p->Hl, p->N, y_map, y_sel, ps);
+    if (pl.mode == PKV_SHARD_HEAD) {
+        StageRange r_x("pkv.exchange");
+        exchange_scores(p->comm, pl, p->Hl, p->N, y_map, y_sel, ps);
+    }
     if (ts != ps) {
         if (!p->ev) PKV_CUDA(cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming));
         PKV_CUDA(cudaEventRecord(p->ev, ps));
@@ -217,8 +224,12 @@ void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, con
     if (slices == 0) return;
     if (arr) PKV_CUDA(cudaStreamWaitEvent(ts, arr->ev_kv, 0));
     // (3) Top-K per (target layer, head): ascending retained indices
-    launch_topk_select(y_sel, slices, p->N, p->K, nullptr, idx, ts);
+    {
+        StageRange r_sel("pkv.select");
+        launch_topk_select(y_sel, slices, p->N, p->K, nullptr, idx, ts);
+    }
     // (4) packed KV gather
+    StageRange r_cmp("pkv.compact");
     launch_compact_kv(kt, vt, idx, slices, p->N, p->K, p->dt * 2, k_out, v_out, p->ctx->sm_count, ts);
     count_launch(p->ctx, 2);
 }

@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(P1<D>::kThreads, 1)
                 L += pm.y * ex2(pm.x - M);
             }
             // fixed reference far above the row's scores: the exact kernel redoes the tile
-            if (kFixed && !(L >= 0x1p-40f)) tile_flags[tile_id] = 1u;
+            if (kFixed && !(L >= 0x1p-40f)) atomicOr(&tile_flags[tile_id], 1u);  // any row flags the tile
             const float lse2 = M + __log2f(L);  // log2 Σ exp2(c·s)
             const int64_t row = (int64_t)qslab * Nq + q;
             if (lse_out) lse_out[row] = lse2 / kLog2e;
