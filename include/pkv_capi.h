@@ -165,6 +165,14 @@ pkv_status pkv_compact_kv(pkv_ctx ctx, const void* k_in_dev, const void* v_in_de
                           int64_t slices, int64_t n, int64_t k, int64_t d, int64_t elem_bytes, void* k_out_dev,
                           void* v_out_dev, void* stream);
 
+/* Select + compaction in one call (topk_indices / apply_mask,
+ * pruning.cpp:20-56,197-215, followed by the packed gather above): writes the
+ * ascending retained indices idx_asc [slices, k] and the packed K/V exactly as
+ * pkv_topk_select then pkv_compact_kv (the two kernels, stream-ordered). */
+pkv_status pkv_select_compact(pkv_ctx ctx, const float* scores_dev, int64_t slices, int64_t n, int64_t k,
+                              const void* k_in_dev, const void* v_in_dev, int64_t d, int64_t elem_bytes,
+                              int32_t* idx_asc_dev, void* k_out_dev, void* v_out_dev, void* stream);
+
 /* The same gather into a paged cache: row j of slice
  * s goes to page block_table[s * max_blocks + j / page_size], row
  * j % page_size, of the pools k_pool / v_pool [pages, page_size, d]. */

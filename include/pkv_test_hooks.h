@@ -27,6 +27,12 @@ pkv_status pkv_test_gemm(pkv_ctx ctx, const float* a_dev, int64_t M, int64_t K, 
 pkv_status pkv_test_attention(pkv_ctx ctx, const float* qkv_dev, int64_t nwin, int64_t Lw, int64_t D, int64_t heads,
                               float* out_dev, void* stream);
 
+/* Select path override for tests: -1 default (the streaming select for rows
+ * of >= 4096 scores; PKV_SELECT_STREAM env), 0 the register-cached radix
+ * kernel (select.cu), 1 the streaming kernel (select_stream.cu) at every
+ * size. Returns the previous setting. */
+int pkv_test_select_path(int mode);
+
 #ifdef __cplusplus
 }
 #endif

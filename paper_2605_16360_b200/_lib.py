@@ -99,6 +99,8 @@ SIGNATURES = {
     "pkv_loss_total": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp, ctypes.c_int, _c_vp, ctypes.c_uint64, _c_vp, _c_vp,
                                       _c_vp]),
     "pkv_slice_metrics": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),
+    "pkv_select_compact": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_i64, _c_i64, _c_vp,
+                                          _c_vp, _c_vp, _c_vp]),
     "pkv_compact_kv": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_vp,
                                       _c_vp, _c_vp]),
     "pkv_score": (ctypes.c_int, [_c_vp, _c_vp, _c_vp] + [_c_i64] * 6 + [_c_u32, _c_vp, _c_vp, _c_vp]),

@@ -155,6 +155,10 @@ __global__ void __launch_bounds__(kThreads, 2 / kTiles)
                 tma_load_3d(sK + st * kKVBytes, &tkv, &kv_full[st], D + head * kD, j * kBK, win);
                 tma_load_3d(sV + st * kKVBytes, &tkv, &kv_full[st], 2 * D + head * kD, j * kBK, win);
             }
+            // drain: observe the last stages' release too (every mbarrier phase
+            // the MMA warps complete is waited on before the CTA exits)
+            for (int j = n_kv > kStages ? n_kv - kStages : 0; j < n_kv; ++j)
+                mbar_wait(&kv_empty[j % kStages], (j / kStages) & 1);
         }
     } else if (warp <= kTiles) {
         // MMA issuer of tile t = warp - 1

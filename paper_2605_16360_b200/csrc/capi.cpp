@@ -240,6 +240,25 @@ pkv_status pkv_compact_kv(pkv_ctx ctx, const void* k_in_dev, const void* v_in_de
     });
 }
 
+pkv_status pkv_select_compact(pkv_ctx ctx, const float* scores_dev, int64_t slices, int64_t n, int64_t k,
+                              const void* k_in_dev, const void* v_in_dev, int64_t d, int64_t elem_bytes,
+                              int32_t* idx_asc_dev, void* k_out_dev, void* v_out_dev, void* stream) {
+    return guard([&] {
+        require_ctx(ctx);
+        PKV_REQUIRE_SHAPE(slices >= 0 && n > 0 && d > 0, "select_compact extents must be positive");
+        PKV_REQUIRE_VALUE(k >= 1 && k <= n, "top-k count ", k, " out of range for length ", n);
+        PKV_REQUIRE_VALUE(n < (int64_t(1) << 31), "token axis too long: ", n);
+        PKV_REQUIRE_VALUE(elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4, "elem_bytes must be 1, 2 or 4");
+        PKV_REQUIRE_VALUE((d * elem_bytes) % 2 == 0, "row bytes must be even");
+        PKV_REQUIRE_VALUE(idx_asc_dev != nullptr, "select_compact needs the index output");
+        auto st = static_cast<cudaStream_t>(stream);
+        launch_topk_select(scores_dev, slices, n, k, nullptr, idx_asc_dev, st);
+        launch_compact_kv(k_in_dev, v_in_dev, idx_asc_dev, slices, n, k, d * elem_bytes, k_out_dev, v_out_dev,
+                          ctx->sm_count, st);
+        count_launch(ctx, 2);
+    });
+}
+
 pkv_status pkv_compact_kv_paged(pkv_ctx ctx, const void* k_in_dev, const void* v_in_dev, const int32_t* idx_asc_dev,
                                 int64_t slices, int64_t n, int64_t k, int64_t d, int64_t elem_bytes,
                                 const int32_t* block_table_dev, int64_t max_blocks, int64_t page_size,

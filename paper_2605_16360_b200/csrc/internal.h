@@ -111,6 +111,11 @@ void check_launch(const char* what);
 // ---------------------------------------------------------- kernel entries
 void launch_topk_select(const float* scores, int64_t slices, int64_t n, int64_t k, uint8_t* mask, int32_t* idx,
                         cudaStream_t st);
+// Streaming select with candidate compaction (select_stream.cu), taken by
+// launch_topk_select for long L2-resident rows (select_stream_eligible).
+bool select_stream_eligible(int64_t slices, int64_t n);
+void launch_topk_select_stream(const float* scores, int64_t slices, int64_t n, int64_t k, uint8_t* mask,
+                               int32_t* idx, cudaStream_t st);
 void launch_topk_select_f64(const double* scores, int64_t slices, int64_t n, int64_t k, uint8_t* mask, int32_t* idx,
                             cudaStream_t st);
 void launch_compact_kv(const void* kin, const void* vin, const int32_t* idx, int64_t slices, int64_t n, int64_t k,

@@ -389,6 +389,10 @@ __global__ void __launch_bounds__(kT, 1024 / kT)
 void launch_topk_select(const float* scores, int64_t slices, int64_t n, int64_t k, uint8_t* mask, int32_t* idx,
                         cudaStream_t st) {
     if (slices == 0) return;
+    if (select_stream_eligible(slices, n)) {
+        launch_topk_select_stream(scores, slices, n, k, mask, idx, st);
+        return;
+    }
     // vector loads / stores only where the caller's pointers allow them (a view
     // with a storage offset, or a row inside a larger buffer, may not)
     const bool a16 = (reinterpret_cast<uintptr_t>(scores) & 15) == 0;

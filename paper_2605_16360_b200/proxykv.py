@@ -22,7 +22,7 @@ from ._lib import (BadMagicError, ConfigError, CudaError, IoError, NoDeviceError
 
 __all__ = [
     "Context", "PruneMask", "MaskApplication", "ModelGeometry", "MapperConfig", "Mapper", "Pruner",
-    "retention_count", "topk_select", "topk_indices", "topk_mask", "apply_mask", "compact_kv", "score", "score_lse",
+    "retention_count", "topk_select", "topk_indices", "topk_mask", "apply_mask", "compact_kv", "select_compact", "score", "score_lse",
     "proxy_prefill_attention", "packed_decode_attention", "paged_decode_attention", "compact_kv_paged", "topk_overlap_device", "captured_mass_device",
     "spearman_device", "slice_metrics_device", "MetricAccumulator", "MetricReport",
     "LossConfig", "LossReport", "loss_total",
@@ -386,6 +386,25 @@ def compact_kv(k_in, v_in, idx_asc, *, ctx: Context = None, stream=None, out=Non
     check(lib().pkv_compact_kv(ctx.h, _ptr(k_in), _ptr(v_in), _ptr(idx_asc), S, n, k, d, k_in.element_size(),
                                _ptr(ko), _ptr(vo), _stream(stream)))
     return ko, vo
+
+
+def select_compact(scores, k_in, v_in, k: int, *, ctx: Context = None, stream=None, out=None):
+    """Top-K select then the packed gather in one call (pkv_select_compact): scores fp32 [S, n],
+    k_in/v_in [S, n, d] cuda -> (idx_asc i32 [S, k], k_out, v_out [S, k, d])."""
+    torch = _torch()
+    ctx = ctx or Context.default(scores.device.index or 0)
+    S, n, d = k_in.shape
+    if tuple(scores.shape) != (S, n) or scores.dtype != torch.float32 or not scores.is_contiguous():
+        raise ShapeError("select_compact expects contiguous float32 scores [S, n] matching k_in")
+    if out is None:
+        idx = torch.empty((S, k), dtype=torch.int32, device=scores.device)
+        ko = torch.empty((S, k, d), dtype=k_in.dtype, device=k_in.device)
+        vo = torch.empty((S, k, d), dtype=v_in.dtype, device=v_in.device)
+    else:
+        idx, ko, vo = out
+    check(lib().pkv_select_compact(ctx.h, _ptr(scores), S, n, k, _ptr(k_in), _ptr(v_in), d, k_in.element_size(),
+                                   _ptr(idx), _ptr(ko), _ptr(vo), _stream(stream)))
+    return idx, ko, vo
 
 
 # ----------------------------------------------------------------- scoring --

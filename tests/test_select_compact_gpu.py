@@ -17,6 +17,25 @@ def pr():
     return np.load(os.path.join(GOLD, "pruning.npz"))
 
 
+def _set_path(mode):
+    import ctypes
+    import paper_2605_16360_b200 as P
+    f = P.lib().pkv_test_select_path
+    f.restype, f.argtypes = ctypes.c_int, [ctypes.c_int]
+    return f(mode)
+
+
+# every test of this module runs on both select kernels, each forced at every
+# size: the register-cached radix kernel (select.cu) and the streaming one with
+# candidate compaction (select_stream.cu; the library's choice for rows longer
+# than 32768 whose score tensor fits in L2)
+@pytest.fixture(autouse=True, params=[0, 1], ids=["cached_radix", "streaming"])
+def select_path(request):
+    prev = _set_path(request.param)
+    yield request.param
+    _set_path(prev)
+
+
 def _sel(scores_np, k, ctx):
     import torch
     import paper_2605_16360_b200 as P
@@ -122,3 +141,55 @@ def test_compaction_bit_exact(gpu, S, n, k, d, dtype):
     eko, evo = O.compact_kv(kb, vb, idx.cpu().numpy())
     np.testing.assert_array_equal(ko.view(torch.int16).cpu().numpy().view(np.uint16), eko)
     np.testing.assert_array_equal(vo.view(torch.int16).cpu().numpy().view(np.uint16), evo)
+
+
+@pytest.mark.parametrize("S,n,rho,d,kind", [(256, 32768, 0.2, 128, "uniform"), (16, 20000, 0.1, 64, "ties"),
+                                            (3, 8193, 0.5, 128, "allequal"), (5, 4099, 0.3, 64, "signed0"),
+                                            (2, 170000, 0.2, 128, "logits"), (4, 1000, 0.2, 64, "uniform"),
+                                            (9, 16387, 0.37, 8, "ties")])
+def test_select_compact(gpu, S, n, rho, d, kind):
+    """pkv_select_compact == oracle select + oracle gather, bit for bit (indices and packed rows)."""
+    import torch
+    import paper_2605_16360_b200 as P
+    r = np.random.RandomState(S * 7 + n)
+    if kind == "uniform":
+        s = r.uniform(0, 1, (S, n))
+    elif kind == "ties":
+        s = np.floor(r.uniform(0, 8, (S, n))) / 8
+    elif kind == "allequal":
+        s = np.full((S, n), 0.25)
+    elif kind == "signed0":
+        s = r.choice([0.0, -0.0, 1e-40, -1e-40, 1.0, -1.0], (S, n))
+    else:
+        s = r.standard_normal((S, n)) * 3
+    s = s.astype(np.float32)
+    k = O.retention_count(rho, n)
+    g = torch.Generator(device="cuda").manual_seed(n)
+    kin = torch.randint(-(1 << 15), 1 << 15, (S, n, d), device="cuda", dtype=torch.int32, generator=g).to(torch.int16)
+    vin = torch.randint(-(1 << 15), 1 << 15, (S, n, d), device="cuda", dtype=torch.int32, generator=g).to(torch.int16)
+    idx, ko, vo = P.select_compact(torch.from_numpy(s).cuda(), kin, vin, k, ctx=gpu)
+    torch.cuda.synchronize()
+    _, oidx = O.topk_select(s, k)
+    np.testing.assert_array_equal(idx.cpu().numpy(), oidx)
+    kb, vb = kin.cpu().numpy().view(np.uint16), vin.cpu().numpy().view(np.uint16)
+    eko, evo = O.compact_kv(kb, vb, oidx)
+    np.testing.assert_array_equal(ko.cpu().numpy().view(np.uint16), eko)
+    np.testing.assert_array_equal(vo.cpu().numpy().view(np.uint16), evo)
+
+
+def test_repeated_calls_and_offset_views(gpu):
+    """Many calls of changing geometry in a row, misaligned (storage-offset) score
+    pointers (scalar-load paths), all vs the oracle."""
+    import torch
+    import paper_2605_16360_b200 as P
+    r = np.random.RandomState(3)
+    for it, (S, n) in enumerate([(4, 9000), (64, 32768), (4, 9000), (1, 70001), (300, 4096), (4, 9000)]):
+        s = r.uniform(0, 1, (S, n)).astype(np.float32)
+        k = O.retention_count(0.2 + 0.05 * it, n)
+        big = torch.zeros(S * n + 3, device="cuda")
+        view = big[1:1 + S * n].view(S, n)  # 4-byte aligned only
+        view.copy_(torch.from_numpy(s).cuda())
+        mask, idx = P.topk_select(view, k, ctx=gpu)
+        omask, oidx = O.topk_select(s, k)
+        np.testing.assert_array_equal(mask.cpu().numpy(), omask)
+        np.testing.assert_array_equal(idx.cpu().numpy(), oidx)

@@ -1,7 +1,8 @@
 """BASELINE.json configs[4]: KV-budget sweep (rho 10-50% x ctx 8k-128k) on
 Llama-3.1-8B target shapes (32 layers x 8 KV heads, head_dim 128, bf16): the
 select + compaction regime, HBM-bound. Per point: select (radix Top-K ->
-ascending indices) and compaction (packed K/V gather) timed with CUDA events
+ascending indices, the library's choice of kernel, and each of the two select
+kernels forced for comparison) and compaction (packed K/V gather) timed with CUDA events
 on the launching stream through the C ABI with preallocated outputs (20 / 10
 back-to-back launches queued behind a spin kernel, after 3 warm-ups; inputs >
 L2 except the scores at 8k-16k, which the select reads once), algorithmic bytes per
@@ -10,6 +11,7 @@ SURVEY.md §8(d), fraction of MEASURED_PEAKS.json HBM bandwidth.
     python tools/bench_sweep.py [--out profiles/r01_sweep.json]
 """
 import argparse
+import ctypes
 import json
 import os
 import sys
@@ -29,6 +31,9 @@ Ll, Hl, dt = 32, 8, 128
 S = Ll * Hl
 hbm = bench.peaks()[0]
 ctx = P.Context(0)
+_hook = P.lib().pkv_test_select_path
+_hook.restype, _hook.argtypes = ctypes.c_int, [ctypes.c_int]
+path = _hook
 st = torch.cuda.current_stream()
 rows = []
 for N in (8192, 16384, 32768, 65536, 131072):
@@ -52,15 +57,23 @@ for N in (8192, 16384, 32768, 65536, 131072):
             cmp()
         t_sel = bench.time_loop(sel, 20, st)
         t_cmp = bench.time_loop(cmp, 10, st)
+        alt = {}
+        for mode, name in ((0, "register_cached_radix"), (1, "streaming")):
+            prev = path(mode)  # force one select kernel (select.cu / select_stream.cu)
+            sel()
+            alt[name] = bench.time_loop(sel, 20, st)
+            path(prev)
         c = dict(Ll=Ll, Hl=Hl, N=N, rho=rho, dt=dt)
         b_sel, b_cmp = bench.bytes_select(c), bench.bytes_compact(c)
         r = dict(N=N, rho=rho, K=K, select_ms=t_sel, compact_ms=t_cmp,
+                 select_kernel_ms=alt,
                  select_gbs=b_sel / t_sel / 1e6, compact_gbs=b_cmp / t_cmp / 1e6,
                  combined_frac_hbm=(b_sel + b_cmp) / (t_sel + t_cmp) / 1e6 / hbm)
         rows.append(r)
-        print(f"N={N:6d} rho={rho:.1f} K={K:6d}  select {t_sel:7.3f} ms {r['select_gbs']:7.0f} GB/s  "
-              f"compact {t_cmp:7.3f} ms {r['compact_gbs']:7.0f} GB/s  select+compact {100 * r['combined_frac_hbm']:.1f}% "
-              f"of {hbm:.0f} GB/s", flush=True)
+        print(f"N={N:6d} rho={rho:.1f} K={K:6d}  select {t_sel * 1e3:6.1f} us (cached radix "
+              f"{alt['register_cached_radix'] * 1e3:6.1f}, streaming {alt['streaming'] * 1e3:6.1f}) "
+              f"{r['select_gbs']:5.0f} GB/s  compact {t_cmp:6.3f} ms {r['compact_gbs']:5.0f} GB/s  "
+              f"select+compact {100 * r['combined_frac_hbm']:.1f}% of {hbm:.0f} GB/s", flush=True)
         del ko, vo, idx
     del scores, kt, vt
     torch.cuda.empty_cache()

@@ -14,10 +14,10 @@ for tool in memcheck racecheck synccheck initcheck; do
   extra=""
   [ "$tool" = "racecheck" ] && extra="--racecheck-report all"
   echo "== $tool: smoke" > "$OUT/sanitizer_$tool.log"
-  eval timeout 1500 $CS --tool $tool $extra $SMOKE >> "$OUT/sanitizer_$tool.log" 2>&1
+  eval timeout 480 $CS --tool $tool $extra $SMOKE >> "$OUT/sanitizer_$tool.log" 2>&1
   echo "exit=$?" >> "$OUT/sanitizer_$tool.log"
 done
 echo "== memcheck: parity tests" >> "$OUT/sanitizer_memcheck.log"
-timeout 2400 $CS --tool memcheck python -m pytest -q -x tests/test_pruner_gpu.py tests/test_score_gpu.py \
+timeout 900 $CS --tool memcheck python -m pytest -q -x tests/test_pruner_gpu.py tests/test_score_gpu.py \
   tests/test_kernels_gpu.py tests/test_decode_gpu.py tests/test_select_f64_gpu.py >> "$OUT/sanitizer_memcheck.log" 2>&1
 echo "exit=$?" >> "$OUT/sanitizer_memcheck.log"
