@@ -25,6 +25,7 @@
 
 #include <mutex>
 
+#include "lse_chunk.cuh"
 #include "score.cuh"
 #include "sm100.cuh"
 
@@ -156,43 +157,6 @@ __device__ __forceinline__ void lse_chunk(const uint32_t (&ra)[32], const uint32
 // the row, so no running max, no max tree and no rescale): all exponents are
 // <= 0 and the sum keeps full relative precision as long as the row's largest
 // term is not far below 1 (checked by the caller).
-template <int kPolyPairs>
-__device__ __forceinline__ float lse_chunk_fixed(const uint32_t (&ra)[32], const uint32_t (&rb)[32], int valid,
-                                                 uint64_t cc, uint64_t nm, uint64_t mp) {
-    const bool masked = __any_sync(0xffffffffu, valid < 64);
-    uint64_t acc0 = pack2(0.0f, 0.0f), acc1 = acc0;
-    if (!masked) {
-#pragma unroll
-        for (int pr = 0; pr < 32; ++pr) {
-            const uint64_t s2 = pr < 16 ? pack2(__uint_as_float(ra[2 * pr]), __uint_as_float(ra[2 * pr + 1]))
-                                        : pack2(__uint_as_float(rb[2 * pr - 32]), __uint_as_float(rb[2 * pr - 31]));
-            uint64_t e;
-            if (((pr + 1) * kPolyPairs) / 32 != (pr * kPolyPairs) / 32) {
-                e = ex2_poly2_fused(s2, cc, mp);
-            } else {
-                const float2 x = unpack2(ffma2(s2, cc, nm));
-                e = pack2(ex2(x.x), ex2(x.y));
-            }
-            if (pr & 1) acc1 = fadd2(acc1, e);
-            else acc0 = fadd2(acc0, e);
-        }
-    } else {
-#pragma unroll
-        for (int pr = 0; pr < 32; ++pr) {
-            float a = pr < 16 ? __uint_as_float(ra[2 * pr]) : __uint_as_float(rb[2 * pr - 32]);
-            float b = pr < 16 ? __uint_as_float(ra[2 * pr + 1]) : __uint_as_float(rb[2 * pr - 31]);
-            a = 2 * pr < valid ? a : -INFINITY;
-            b = 2 * pr + 1 < valid ? b : -INFINITY;
-            const float2 x = unpack2(ffma2(pack2(a, b), cc, nm));
-            const uint64_t e = pack2(ex2(x.x), ex2(x.y));
-            if (pr & 1) acc1 = fadd2(acc1, e);
-            else acc0 = fadd2(acc0, e);
-        }
-    }
-    const float2 ssum = unpack2(fadd2(acc0, acc1));
-    return ssum.x + ssum.y;
-}
-
 // max_k |k| per (layer, KV head) slab: the Cauchy–Schwarz score bound's K side
 __global__ void kmax_norm_kernel(const __nv_bfloat16* __restrict__ k, int64_t rows, int d, float* __restrict__ out) {
     const int64_t slab = blockIdx.x;
@@ -326,7 +290,7 @@ __global__ void __launch_bounds__(P1<D>::kThreads, 1)
         const int kmax_k = causal ? (q + off + 1 < Nk ? q + off + 1 : Nk) : Nk;  // keys [0, kmax_k) allowed
         float m = -INFINITY, lsum = 0.0f;  // m in the log2 (scaled) domain
         constexpr int kChunks = C::kSegCols / 64;
-        uint64_t fcc = 0, fnm = 0, fmp = 0;
+        float fnm = 0.0f, fmp = 0.0f;
         for (int j = 0; j < n_kv; ++j) {
             const int sb = j & 1;
             mbar_wait(&s_full[sb], (j >> 1) & 1);
@@ -347,9 +311,8 @@ __global__ void __launch_bounds__(P1<D>::kThreads, 1)
                         }
                     }
                 m = ceilf(c_log2 * sqrtf(qn2) * __ldg(kmax + kslab)) + 1.0f;
-                fcc = pack2(c_log2, c_log2);
-                fnm = pack2(-m, -m);
-                fmp = pack2(12582912.0f - m, 12582912.0f - m);
+                fnm = -m;
+                fmp = 12582912.0f - m;
             }
             const uint32_t base = tmem + ((quad * 32) << 16) + sb * C::kBK + seg * C::kSegCols;
             uint32_t ra[32], rb[32];
@@ -368,8 +331,8 @@ __global__ void __launch_bounds__(P1<D>::kThreads, 1)
                     if (lane == 0) mbar_arrive(&s_empty[sb]);
                 }
                 if (kFixed)
-                    lsum += lse_chunk_fixed<kPolyPairs>(ra, rb, kmax_k - (j * C::kBK + seg * C::kSegCols + 64 * c),
-                                                        fcc, fnm, fmp);
+                    lsum += lse_chunk_fixed<kPolyPairs, D>(ra, rb, kmax_k - (j * C::kBK + seg * C::kSegCols + 64 * c),
+                                                           fnm, fmp);
                 else
                     lse_chunk<kPolyPairs>(ra, rb, kmax_k - (j * C::kBK + seg * C::kSegCols + 64 * c), c_log2, m,
                                           lsum);
@@ -626,23 +589,25 @@ void run_lse(const ScoreShape& s, const void* q, const void* k, float* lse, __nv
     static std::atomic<uint64_t> once{0};
     static int poly = 10;
     using KernT = decltype(&score_lse_kernel<D, 12, false>);
-    static KernT table[2][5] = {{score_lse_kernel<D, 6, false>, score_lse_kernel<D, 8, false>,
+    static KernT table[2][7] = {{score_lse_kernel<D, 6, false>, score_lse_kernel<D, 8, false>,
                                  score_lse_kernel<D, 10, false>, score_lse_kernel<D, 12, false>,
-                                 score_lse_kernel<D, 14, false>},
+                                 score_lse_kernel<D, 14, false>, score_lse_kernel<D, 16, false>,
+                                 score_lse_kernel<D, 18, false>},
                                 {score_lse_kernel<D, 6, true>, score_lse_kernel<D, 8, true>,
                                  score_lse_kernel<D, 10, true>, score_lse_kernel<D, 12, true>,
-                                 score_lse_kernel<D, 14, true>}};
+                                 score_lse_kernel<D, 14, true>, score_lse_kernel<D, 16, true>,
+                                 score_lse_kernel<D, 18, true>}};
     if (first_on_device(once)) {
         for (auto& row : table)
             for (KernT kf : row) set_smem(kf, C::kSmem);
-        if (const char* e = getenv("PKV_POLY_PAIRS")) poly = atoi(e);  // tuning knob: 6..14 of 32 pairs
+        if (const char* e = getenv("PKV_POLY_PAIRS")) poly = atoi(e);  // tuning knob: 6..18 of 32 pairs
     }
     const CUtensorMap tq = make_tmap_3d(q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, s.Nq, s.L * s.Hq, D * 2, D * 2 * s.Nq,
                                         64, C::kBQ, 1, CU_TENSOR_MAP_SWIZZLE_128B);
     const CUtensorMap tk = make_tmap_3d(k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, s.Nk, s.L * s.Hkv, D * 2, D * 2 * s.Nk,
                                         64, C::kBK, 1, CU_TENSOR_MAP_SWIZZLE_128B);
     const dim3 grid((unsigned)((s.Nq + C::kBQ - 1) / C::kBQ), (unsigned)s.Hq, (unsigned)s.L);
-    const int pi = poly <= 6 ? 0 : poly <= 8 ? 1 : poly <= 10 ? 2 : poly <= 12 ? 3 : 4;
+    const int pi = poly <= 6 ? 0 : poly <= 8 ? 1 : poly <= 10 ? 2 : poly <= 12 ? 3 : poly <= 14 ? 4 : poly <= 16 ? 5 : 6;
     const float c = kLog2e / sqrtf((float)D);
     if (kmax) {  // fixed-reference pass, then the exact kernel on the flagged tiles only
         table[1][pi]<<<grid, C::kThreads, C::kSmem, st>>>(tq, tk, (int)s.Hq, (int)s.Hkv, (int)s.Nq, (int)s.Nk,

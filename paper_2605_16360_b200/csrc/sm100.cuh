@@ -270,6 +270,55 @@ __device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
     return d;
 }
 
+// Broadcast-operand forms: a scalar duplicated into both halves inside the asm
+// lets ptxas encode it as a .F32 broadcast register or an immediate, so the
+// FFMA2 reads 3-4 32-bit registers instead of 6 (measured: 6-register FFMA2
+// issues every 3 cycles per SMSP, 4-register ones every 2; tools/probe_exp.cu).
+// a2 * b + c, b and c scalars
+__device__ __forceinline__ uint64_t ffma2_ss(uint64_t a, float b, float c) {
+    uint64_t d;
+    asm("{.reg .b64 bb, cc;\n\tmov.b64 bb, {%2, %2};\n\tmov.b64 cc, {%3, %3};\n\t"
+        "fma.rn.f32x2 %0, %1, bb, cc;}"
+        : "=l"(d)
+        : "l"(a), "f"(b), "f"(c));
+    return d;
+}
+// a2 * b + c2, b scalar
+__device__ __forceinline__ uint64_t ffma2_sp(uint64_t a, float b, uint64_t c) {
+    uint64_t d;
+    asm("{.reg .b64 bb;\n\tmov.b64 bb, {%2, %2};\n\tfma.rn.f32x2 %0, %1, bb, %3;}" : "=l"(d) : "l"(a), "f"(b), "l"(c));
+    return d;
+}
+// a2 * b2 + c, c scalar
+__device__ __forceinline__ uint64_t ffma2_ps(uint64_t a, uint64_t b, float c) {
+    uint64_t d;
+    asm("{.reg .b64 cc;\n\tmov.b64 cc, {%3, %3};\n\tfma.rn.f32x2 %0, %1, %2, cc;}" : "=l"(d) : "l"(a), "l"(b), "f"(c));
+    return d;
+}
+// a - b2, a scalar
+__device__ __forceinline__ uint64_t fsub2_s(float a, uint64_t b) {
+    uint64_t d;
+    asm("{.reg .b64 aa;\n\tmov.b64 aa, {%1, %1};\n\tsub.rn.f32x2 %0, aa, %2;}" : "=l"(d) : "f"(a), "l"(b));
+    return d;
+}
+
+// ex2_poly2_fused with scalar c (ideally a compile-time constant: an FFMA2
+// immediate) and mp = 1.5·2^23 − m: 2^(c·s − m) for both halves of s2.
+__device__ __forceinline__ uint64_t ex2_poly2_fused_s(uint64_t s2, float c, float mp) {
+    uint64_t t = ffma2_ss(s2, c, mp);
+    float2 tf = unpack2(t);
+    tf.x = fmaxf(tf.x, 12582912.0f - 125.0f);
+    tf.y = fmaxf(tf.y, 12582912.0f - 125.0f);
+    t = pack2(tf.x, tf.y);
+    const uint64_t f = ffma2_sp(s2, c, fsub2_s(mp, t));
+    uint64_t p = ffma2_ss(f, 0.05508868396282196f, 0.24260404706001282f);
+    p = ffma2_ps(p, f, 0.6932762265205383f);
+    p = ffma2_ps(p, f, 0.9999289512634277f);
+    const float2 pf = unpack2(p);
+    return pack2(__int_as_float((__float_as_int(tf.x) << 23) + __float_as_int(pf.x)),
+                 __int_as_float((__float_as_int(tf.y) << 23) + __float_as_int(pf.y)));
+}
+
 // Two 2^x (x <= 0) on the FMA pipe with packed FADD2/FFMA2 (see ex2_poly).
 __device__ __forceinline__ uint64_t ex2_poly2(uint64_t x2) {
     float2 x = unpack2(x2);

@@ -122,6 +122,31 @@ __global__ void bench(int iters, uint32_t* out, long long* cycles) {
                 asm volatile("fma.rn.f32 %0, %1, %2, %3;" : "=f"(f[j]) : "f"(f[j]), "f"(f[(j + 1) % CHAINS]), "f"(f[(j + 2) % CHAINS]));
                 asm volatile("fma.rn.f32 %0, %1, %2, %3;" : "=r"(a[j]) : "r"(a[j]), "r"(a[(j + 1) % CHAINS]), "r"(a[(j + 2) % CHAINS]));
                 a[(j + 3) % CHAINS] = __float_as_uint(op_ex2_f32(__uint_as_float(a[(j + 3) % CHAINS])));
+            } else if (OP == 23) {  // cvt.rn.bf16x2.f32 (F2FP.BF16 pack)
+                uint32_t r;
+                asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(f[j]), "f"(__uint_as_float(a[j])));
+                a[j] = r;
+            } else if (OP == 24) {  // MUFU + bf16x2 pack, independent (per pair)
+                uint32_t r;
+                asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(__uint_as_float(a[j])), "f"(__uint_as_float(a[(j + 1) % CHAINS])));
+                a[j] = r;
+                f[j] = op_ex2_f32(f[j]);
+            } else if (OP == 25) {  // FFMA2 + bf16x2 pack, independent (per pair)
+                uint64_t r;
+                asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(d[j]), "l"(d[(j + 1) % CHAINS]), "l"(d[(j + 2) % CHAINS]));
+                d[j] = r;
+                uint32_t q;
+                asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(q) : "f"(__uint_as_float(a[j])), "f"(__uint_as_float(a[(j + 1) % CHAINS])));
+                a[j] = q;
+            } else if (OP == 26) {  // 2 MUFU + FFMA2 + bf16x2 pack (per pair of exps: the MMA-summed softmax step)
+                uint64_t r;
+                asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(d[j]), "l"(d[(j + 1) % CHAINS]), "l"(d[(j + 2) % CHAINS]));
+                d[j] = r;
+                f[j] = op_ex2_f32(f[j]);
+                a[(j + 3) % CHAINS] = __float_as_uint(op_ex2_f32(__uint_as_float(a[(j + 3) % CHAINS])));
+                uint32_t q;
+                asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(q) : "f"(__uint_as_float(a[j])), "f"(f[(j + 1) % CHAINS]));
+                a[j] ^= q;
             } else if (OP == 10) {  // HFMA2 with fp32-pair output? (fma.rn.f32x2 fed from f16 is not a thing) -> F2F pair
                 uint64_t r;
                 asm volatile(
@@ -186,5 +211,9 @@ int main() {
     run<20>("FADD2 distinct regs", 2);
     run<21>("FFMA2 distinct + MUFU (/pair)", 1);
     run<22>("2 FFMA distinct + MUFU (/trio)", 1);
+    run<23>("cvt.rn.bf16x2.f32", 2);
+    run<24>("MUFU + bf16x2 pack (/pair)", 1);
+    run<25>("FFMA2 distinct + bf16x2 pack", 1);
+    run<26>("2MUFU+FFMA2+pack (/quad)", 1);
     return 0;
 }
