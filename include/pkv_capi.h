@@ -156,6 +156,33 @@ pkv_status pkv_loss_total(pkv_ctx ctx, const float* logits_dev, const float* y_d
                           const pkv_loss_config* cfg, uint64_t seed, pkv_loss_report* report_out, double* grad_dev,
                           void* stream);
 
+/* ------------------------------------------- mapper training (f-4) ---- */
+/* GPU training of the HybridAxialMapper: the reference's training forward
+ * (forward_pair(x, params, training = true), mapper.cpp:274-342: batchnorm1d
+ * on batch statistics with the running-stat EMA, ops.cpp:806-850) and the
+ * reverse sweep its tape performs (tensor.cpp:156-199 over the op closures of
+ * ops.cpp / mapper.cpp) from d loss / d logits — e.g. pkv_loss_total's
+ * grad_dev — to d loss / d every parameter. fp32 on the device (the
+ * reference is fp64). A trainer owns an fp32 copy of the blob
+ * (pkv_mapper_init_params layout: named_parameters then the BN buffers). */
+typedef struct pkv_trainer_s* pkv_trainer;
+pkv_status pkv_trainer_create(pkv_ctx ctx, const int64_t* geom5, const int64_t* cfg12, const double* blob,
+                              int64_t count, pkv_trainer* out);
+void pkv_trainer_destroy(pkv_trainer t);
+/* params = parameter values (the gradient's length), total = params + BN buffers */
+pkv_status pkv_trainer_param_count(pkv_trainer t, int64_t* params, int64_t* total);
+/* training forward_pair: x fp32 [B, H_s, n] (n <= crop_len) -> logits fp32
+ * [B, H_l, n]; keeps the activations for pkv_trainer_backward and updates the
+ * BN running statistics (ValueError "exceeds crop_len", "needs B*N >= 2"). */
+pkv_status pkv_trainer_forward(pkv_trainer t, const float* x_dev, int64_t B, int64_t n, float* logits_dev,
+                               void* stream);
+/* d loss / d logits (fp64 [B, H_l, n], e.g. pkv_loss_total's grad_dev) of the
+ * last forward -> grad_dev[params] += d loss / d parameters (fp64,
+ * named_parameters order). */
+pkv_status pkv_trainer_backward(pkv_trainer t, const double* dlogits_dev, double* grad_dev, void* stream);
+/* the current blob (parameters + BN running statistics), host fp64 [total] */
+pkv_status pkv_trainer_blob(pkv_trainer t, double* blob_host);
+
 /* --------------------------------------------------- compaction (a-4) ---- */
 /* Packed KV gather in apply_mask order (no reference code; the reference only
  * reports indices, pruning.cpp:197-215): for s < slices, j < k,

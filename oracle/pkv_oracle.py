@@ -605,6 +605,22 @@ class RefLib:
                    global_filtered=int(cnt[3]), cos_floor_hits=int(cnt[4]))
         return out, grad
 
+    def mapper_train_grad(self, m: "RefMapper", x: np.ndarray, dlogits: np.ndarray):
+        """Training-mode forward_pair + the tape's reverse sweep of Σ dlogits ⊙ logits
+        (ref_capi.cpp pkvref_mapper_train_grad): (logits, parameter gradients in
+        named_parameters() order, concatenated). Updates m's BN running statistics."""
+        xx = np.ascontiguousarray(x, np.float64)
+        b, hs, n = xx.shape
+        dl = np.ascontiguousarray(dlogits, np.float64)
+        logits = np.zeros_like(dl)
+        nparam = sum(t.size for name, t in m.tensors() if not name.endswith(("running_mean", "running_var")))
+        grads = np.zeros(nparam, np.float64)
+        self.L.pkvref_mapper_train_grad.argtypes = [ctypes.c_void_p, _f64p, ctypes.c_int64, ctypes.c_int64,
+                                                    ctypes.c_int64, _f64p, _f64p, _f64p]
+        self._check(self.L.pkvref_mapper_train_grad(m.h, _ptr(xx, _f64p), b, hs, n, _ptr(dl, _f64p),
+                                                    _ptr(logits, _f64p), _ptr(grads, _f64p)))
+        return logits, grads
+
     def apply_mask(self, bits: np.ndarray, k: int, head_dim: int, bytes_per_elem: int = 2):
         b = np.ascontiguousarray(bits, np.uint8)
         shape = np.array(b.shape, np.int64)
@@ -699,6 +715,10 @@ class RefMapper:
         out = np.zeros((B, self.g.target_heads, n))
         self.ref._check(self.ref.L.pkvref_forward_pair(self.h, _ptr(x, _f64p), B, hs, n, _ptr(out, _f64p)))
         return out
+
+    def train_grad(self, x: np.ndarray, dlogits: np.ndarray):
+        """(logits, parameter gradients) of one training step; see RefLib.mapper_train_grad."""
+        return self.ref.mapper_train_grad(self, x, dlogits)
 
     def sliding_forward(self, x: np.ndarray) -> np.ndarray:
         x = np.ascontiguousarray(x, np.float64)

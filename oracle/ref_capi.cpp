@@ -308,6 +308,40 @@ int pkvref_forward_full(void* h, const double* x, int64_t b, int64_t ls, int64_t
     });
 }
 
+// Training step of the mapper (mapper.cpp:274-342 with training = true:
+// batchnorm1d on batch statistics + the running-stat EMA, ops.cpp:806-850),
+// then the tape's reverse sweep (tensor.cpp) of L = Σ dlogits ⊙ logits, i.e.
+// the parameter gradients for an upstream gradient dlogits [B, H_l, n].
+// grads_out: every named_parameters() tensor's gradient, concatenated in that
+// order (the parameter part of the blob layout). The BN running statistics
+// in the handle are updated as the reference's training forward does.
+int pkvref_mapper_train_grad(void* h, const double* x, int64_t b, int64_t hs, int64_t n, const double* dlogits,
+                             double* logits_out, double* grads_out) {
+    return guard([&] {
+        auto& p = static_cast<RefMapper*>(h)->params;
+        p.set_trainable(true);
+        struct Frozen {
+            MapperParams& p;
+            ~Frozen() { p.set_trainable(false); }
+        } frozen{p};
+        for (auto& nt : p.named_parameters()) nt.second.zero_grad();
+        const int64_t shape[3] = {b, hs, n};
+        const Tensor y = forward_pair(make_tensor(x, shape, 3), p, true);
+        const Tensor dl = Tensor::from_data(y.shape(), std::vector<double>(dlogits, dlogits + y.numel()));
+        const Tensor loss = sum(mul(y, dl));
+        loss.backward();
+        std::memcpy(logits_out, y.data().data(), y.data().size() * sizeof(double));
+        size_t o = 0;
+        for (auto& nt : p.named_parameters()) {
+            const auto& g = nt.second.grad();
+            const size_t cnt = static_cast<size_t>(nt.second.numel());
+            if (g.size() == cnt) std::memcpy(grads_out + o, g.data(), cnt * sizeof(double));
+            else std::memset(grads_out + o, 0, cnt * sizeof(double));
+            o += cnt;
+        }
+    });
+}
+
 // The reference's own Rng (rng.hpp:25-87), for regenerating the test inputs
 // of test_pruning.cpp / test_mapper.cpp in the golden-vector script.
 void* pkvref_rng_create(uint64_t seed) { return new Rng(seed); }

@@ -25,7 +25,7 @@ __all__ = [
     "retention_count", "topk_select", "topk_indices", "topk_mask", "apply_mask", "compact_kv", "select_compact", "score", "score_lse",
     "proxy_prefill_attention", "packed_decode_attention", "paged_decode_attention", "compact_kv_paged", "topk_overlap_device", "captured_mass_device",
     "spearman_device", "slice_metrics_device", "MetricAccumulator", "MetricReport",
-    "LossConfig", "LossReport", "loss_total",
+    "LossConfig", "LossReport", "loss_total", "MapperTrainer",
     "layer_pair", "window_offsets", "mapper_init_params", "ShapeError", "PkvValueError", "ConfigError",
     "CudaError", "NoDeviceError", "PkvError", "SCORE_REDUCE_MAX", "SCORE_REDUCE_SUM", "SCORE_CAUSAL",
     "MAPPER_FP16", "MAPPER_FP16X2", "MAPPER_FP16X3", "SHARD_LAYER", "SHARD_HEAD", "ShardPlan", "shard_plan",
@@ -370,6 +370,59 @@ def loss_total(logits, y, cfg: LossConfig = None, seed: int = 0, *, want_grad: b
                                ctypes.byref(c), ctypes.c_uint64(seed), ctypes.byref(rep),
                                _ptr(grad) if want_grad else None, _stream(stream)))
     return LossReport(*[getattr(rep, f[0]) for f in _CLossReport._fields_]), grad
+
+
+class MapperTrainer:
+    """GPU training of the HybridAxialMapper (pkv_trainer): the reference's training
+    forward_pair (mapper.cpp:274-342, BN on batch statistics) and the reverse sweep
+    of its tape from d loss / d logits to the parameter gradients (blob layout)."""
+
+    def __init__(self, geom: ModelGeometry, cfg: MapperConfig, blob: np.ndarray = None, *, seed: int = 0,
+                 ctx: Context = None):
+        self.geom, self.cfg = geom, cfg
+        self.ctx = ctx or Context.default()
+        if blob is None:
+            blob = mapper_init_params(geom, cfg, seed)
+        blob = np.ascontiguousarray(blob, np.float64)
+        h = ctypes.c_void_p()
+        check(lib().pkv_trainer_create(self.ctx.h, geom.as5(), cfg.as12(), blob.ctypes.data, blob.size,
+                                       ctypes.byref(h)))
+        self.h = h
+        npar, tot = ctypes.c_int64(), ctypes.c_int64()
+        check(lib().pkv_trainer_param_count(h, ctypes.byref(npar), ctypes.byref(tot)))
+        self.n_params, self.n_total = npar.value, tot.value
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h and _lib._lib is not None:
+            _lib._lib.pkv_trainer_destroy(h)
+            self.h = None
+
+    def forward(self, x, stream=None):
+        """x fp32 cuda [B, H_s, n] -> logits fp32 [B, H_l, n] (training mode; keeps activations)."""
+        torch = _torch()
+        B, hs, n = x.shape
+        if hs != self.geom.proxy_heads:
+            raise ShapeError(f"input has {hs} proxy heads, geometry expects {self.geom.proxy_heads}")
+        x = x.contiguous()
+        y = torch.empty((B, self.geom.target_heads, n), dtype=torch.float32, device=x.device)
+        check(lib().pkv_trainer_forward(self.h, _ptr(x), B, n, _ptr(y), _stream(stream)))
+        return y
+
+    def backward(self, dlogits, grad=None, stream=None):
+        """d loss / d logits (fp64 cuda, the last forward's shape) -> parameter gradients
+        (fp64 cuda [n_params], accumulated into `grad` when given)."""
+        torch = _torch()
+        if grad is None:
+            grad = torch.zeros(self.n_params, dtype=torch.float64, device=dlogits.device)
+        check(lib().pkv_trainer_backward(self.h, _ptr(dlogits.contiguous()), _ptr(grad), _stream(stream)))
+        return grad
+
+    def blob(self) -> np.ndarray:
+        """Parameters + BN running statistics (pkv_mapper_init_params layout)."""
+        out = np.zeros(self.n_total, np.float64)
+        check(lib().pkv_trainer_blob(self.h, out.ctypes.data))
+        return out
 
 
 def compact_kv(k_in, v_in, idx_asc, *, ctx: Context = None, stream=None, out=None):
