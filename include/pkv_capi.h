@@ -180,6 +180,9 @@ pkv_status pkv_trainer_forward(pkv_trainer t, const float* x_dev, int64_t B, int
  * last forward -> grad_dev[params] += d loss / d parameters (fp64,
  * named_parameters order). */
 pkv_status pkv_trainer_backward(pkv_trainer t, const double* dlogits_dev, double* grad_dev, void* stream);
+/* host fp64 forms of forward / backward (synchronous; grad_host += d loss / d params) */
+pkv_status pkv_trainer_forward_host(pkv_trainer t, const double* x_host, int64_t B, int64_t n, double* logits_host);
+pkv_status pkv_trainer_backward_host(pkv_trainer t, const double* dlogits_host, double* grad_host);
 /* the current blob (parameters + BN running statistics), host fp64 [total] */
 pkv_status pkv_trainer_blob(pkv_trainer t, double* blob_host);
 

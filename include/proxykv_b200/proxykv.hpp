@@ -282,6 +282,45 @@ private:
     ModelGeometry geom_;
 };
 
+// GPU training (pkv_trainer): the reference's training forward_pair
+// (mapper.cpp:274-342, BN on batch statistics + the running-stat EMA) and the
+// reverse sweep of its tape from d loss / d logits to every parameter
+// gradient (named_parameters order). DEVICE buffers.
+class MapperTrainer {
+public:
+    MapperTrainer(const Context& ctx, const ModelGeometry& g, const MapperConfig& c, const std::vector<double>& blob) {
+        check(pkv_trainer_create(ctx.get(), g.as5().data(), c.as12().data(), blob.data(),
+                                 static_cast<int64_t>(blob.size()), &h_));
+        check(pkv_trainer_param_count(h_, &params_, &total_));
+    }
+    ~MapperTrainer() { pkv_trainer_destroy(h_); }
+    MapperTrainer(const MapperTrainer&) = delete;
+    MapperTrainer& operator=(const MapperTrainer&) = delete;
+    // x [B, H_s, n] fp32 -> logits [B, H_l, n] fp32; keeps the activations
+    void forward(const float* x_dev, int64_t B, int64_t n, float* logits_dev, void* stream = nullptr) {
+        check(pkv_trainer_forward(h_, x_dev, B, n, logits_dev, stream));
+    }
+    // grad_dev[param_count()] += d loss / d params for d loss / d logits (fp64) of the last forward
+    void backward(const double* dlogits_dev, double* grad_dev, void* stream = nullptr) {
+        check(pkv_trainer_backward(h_, dlogits_dev, grad_dev, stream));
+    }
+    // host fp64 forms (synchronous)
+    void forward_host(const double* x, int64_t B, int64_t n, double* logits) {
+        check(pkv_trainer_forward_host(h_, x, B, n, logits));
+    }
+    void backward_host(const double* dlogits, double* grad) { check(pkv_trainer_backward_host(h_, dlogits, grad)); }
+    std::vector<double> blob() const {
+        std::vector<double> b(static_cast<size_t>(total_));
+        check(pkv_trainer_blob(h_, b.data()));
+        return b;
+    }
+    int64_t param_count() const { return params_; }
+
+private:
+    pkv_trainer h_ = nullptr;
+    int64_t params_ = 0, total_ = 0;
+};
+
 // ---- the reference's mapper entry points on host tensors (mapper.hpp:94-126)
 
 // mapper.hpp:67-100: the parameters (the reference initialisation as the flat
@@ -304,9 +343,32 @@ struct MapperParams {
         if (!dev_) dev_ = std::make_shared<Mapper>(default_context(), geometry, config, blob, precision);
         return *dev_;
     }
+    MapperTrainer& trainer() {
+        if (!train_) train_ = std::make_shared<MapperTrainer>(default_context(), geometry, config, blob);
+        return *train_;
+    }
+    // after a training forward: the BN running statistics it updated, back into
+    // `blob` (the eval mapper is rebuilt from them on next use)
+    void sync_from_trainer() {
+        blob = train_->blob();
+        dev_.reset();
+    }
+    // The tape's reverse sweep for the last training forward_pair: d loss / d
+    // every parameter (named_parameters order) for d loss / d logits [B, H_l, n].
+    std::vector<double> backward(const std::vector<double>& dlogits) {
+        if (!train_ || last_logits_ == 0) throw ValueError("backward needs a training forward_pair first");
+        if (static_cast<int64_t>(dlogits.size()) != last_logits_)
+            throw ShapeError("dlogits must match the last training forward's [B, H_l, n]");
+        std::vector<double> g(static_cast<size_t>(train_->param_count()), 0.0);
+        train_->backward_host(dlogits.data(), g.data());
+        return g;
+    }
+    void note_training_forward(int64_t logits) { last_logits_ = logits; }
 
 private:
     std::shared_ptr<Mapper> dev_;
+    std::shared_ptr<MapperTrainer> train_;
+    int64_t last_logits_ = 0;
 };
 
 // mapper.hpp:111-114
@@ -315,16 +377,24 @@ struct StageTrace {
 };
 
 // mapper.hpp:118-119 / mapper.cpp:274-342: x [B, H_s, n] -> raw logits
-// [B, H_l, n], n <= crop_len. training = true is the reference's batch-stat
-// BatchNorm path (training only): not on the GPU prune path -> ValueError.
+// [B, H_l, n], n <= crop_len. training = true runs the reference's training
+// forward on the GPU trainer (BN batch statistics; the running statistics in
+// params.blob are updated) and keeps its activations for params.backward();
+// the trace is an eval-path output.
 inline Tensor forward_pair(const Tensor& x, MapperParams& params, bool training, StageTrace* trace = nullptr) {
     const ModelGeometry& g = params.geometry;
     if (x.dim() != 3) throw ShapeError("forward_pair input must be [B, H_s, N], got " + shape_str(x.shape));
     if (x.size(1) != g.proxy_heads)
         throw ShapeError("input has " + std::to_string(x.size(1)) + " proxy heads, geometry expects " +
                          std::to_string(g.proxy_heads));
-    if (training) throw ValueError("forward_pair(training=true) is the training path; the GPU mapper is eval-only");
     const int64_t B = x.size(0), n = x.size(2);
+    if (training) {
+        Tensor y({B, g.target_heads, n});
+        params.trainer().forward_host(x.data.data(), B, n, y.data.data());
+        params.sync_from_trainer();
+        params.note_training_forward(static_cast<int64_t>(y.data.size()));
+        return y;
+    }
     const int64_t syn = params.config.synthetic_heads > 0 ? params.config.synthetic_heads : g.proxy_heads;
     Tensor y({B, g.target_heads, n});
     const bool want = trace && params.config.stage_cross == StageMode::kActive;

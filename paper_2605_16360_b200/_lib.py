@@ -102,6 +102,8 @@ SIGNATURES = {
     "pkv_trainer_forward": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_vp, _c_vp]),
     "pkv_trainer_backward": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp]),
     "pkv_trainer_blob": (ctypes.c_int, [_c_vp, _c_vp]),
+    "pkv_trainer_forward_host": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_vp]),
+    "pkv_trainer_backward_host": (ctypes.c_int, [_c_vp, _c_vp, _c_vp]),
     "pkv_loss_total": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp, ctypes.c_int, _c_vp, ctypes.c_uint64, _c_vp, _c_vp,
                                       _c_vp]),
     "pkv_slice_metrics": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp]),

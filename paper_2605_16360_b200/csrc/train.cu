@@ -562,10 +562,13 @@ public:
     void backward(const double* dlogits, double* grad, cudaStream_t st);
     void blob(double* out) const;
 
+    int64_t last_logits() const { return have_forward ? B_ * geom.target_heads * n_ : 0; }
+
     pkv_ctx ctx;
     Geometry geom;
     Config cfg;
     int64_t count = 0, nparam = 0;
+    DevBuf host_io;  // staging for the host forms
 
 private:
     const float* p(const std::string& name) const { return P + off.at(name); }
@@ -944,6 +947,37 @@ pkv_status pkv_trainer_backward(pkv_trainer t, const double* dlogits_dev, double
         PKV_REQUIRE_VALUE(t, "null trainer");
         t->t->backward(dlogits_dev, grad_dev, static_cast<cudaStream_t>(stream));
         count_launch(t->t->ctx);
+    });
+}
+
+pkv_status pkv_trainer_forward_host(pkv_trainer t, const double* x_host, int64_t B, int64_t n, double* logits_host) {
+    return guard([&] {
+        PKV_REQUIRE_VALUE(t, "null trainer");
+        Trainer& tr = *t->t;
+        PKV_REQUIRE_SHAPE(B > 0 && n > 0, "forward_pair input must be [B, H_s, N] with positive extents");
+        const size_t nx = static_cast<size_t>(B * tr.geom.proxy_heads * n), ny = static_cast<size_t>(B * tr.geom.target_heads * n);
+        std::vector<float> xf(x_host, x_host + nx), yf(ny);
+        float* d = static_cast<float*>(tr.host_io.get((nx + ny) * sizeof(float)));
+        PKV_CUDA(cudaMemcpy(d, xf.data(), nx * sizeof(float), cudaMemcpyHostToDevice));
+        tr.forward(d, B, n, d + nx, nullptr);
+        PKV_CUDA(cudaMemcpy(yf.data(), d + nx, ny * sizeof(float), cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < ny; ++i) logits_host[i] = yf[i];
+        count_launch(tr.ctx);
+    });
+}
+
+pkv_status pkv_trainer_backward_host(pkv_trainer t, const double* dlogits_host, double* grad_host) {
+    return guard([&] {
+        PKV_REQUIRE_VALUE(t, "null trainer");
+        Trainer& tr = *t->t;
+        const size_t nl = static_cast<size_t>(tr.last_logits()), np = static_cast<size_t>(tr.nparam);
+        PKV_REQUIRE_VALUE(nl > 0, "backward needs a training forward first");
+        double* d = static_cast<double*>(tr.host_io.get((nl + np) * sizeof(double)));
+        PKV_CUDA(cudaMemcpy(d, dlogits_host, nl * sizeof(double), cudaMemcpyHostToDevice));
+        PKV_CUDA(cudaMemcpy(d + nl, grad_host, np * sizeof(double), cudaMemcpyHostToDevice));
+        tr.backward(d, d + nl, nullptr);
+        PKV_CUDA(cudaMemcpy(grad_host, d + nl, np * sizeof(double), cudaMemcpyDeviceToHost));
+        count_launch(tr.ctx);
     });
 }
 

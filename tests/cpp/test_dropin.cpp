@@ -162,7 +162,26 @@ int main() {
         Tensor xl({1, 4, 2049});
         CHECK(throws_with<ValueError>([&] { forward_pair(xl, mp, false); }, "sliding_forward"));
         CHECK(throws<ShapeError>([&] { forward_pair(Tensor({1, 3, 10}), mp, false); }));
-        CHECK(throws<ValueError>([&] { forward_pair(x, mp, true); }));
+        // training forward_pair runs the GPU trainer: BN running statistics move, the eval
+        // path then uses them, and backward() gives every parameter gradient
+        {
+            MapperParams tp = MapperParams::init(mg, mc, 3);
+            const std::vector<double> before = tp.blob;
+            CHECK(throws<ValueError>([&] { tp.backward(std::vector<double>(2 * 8 * 300, 1.0)); }));
+            Tensor yt = forward_pair(x, tp, true);
+            CHECK((yt.shape == Shape{2, 8, 300}));
+            bool finite = true;
+            for (double v : yt.data) finite = finite && std::isfinite(v);
+            CHECK(finite);
+            CHECK(tp.blob != before);  // running statistics updated (ops.cpp:846-849)
+            const std::vector<double> gr = tp.backward(std::vector<double>(yt.data.size(), 1.0 / 4800.0));
+            CHECK(gr.size() + 2 * (256 + 512) == before.size());  // every parameter, no BN buffers
+            double gn = 0.0;
+            for (double v : gr) gn += v * v;
+            CHECK(gn > 0.0 && std::isfinite(gn));
+            CHECK(throws<ShapeError>([&] { tp.backward(std::vector<double>(3, 0.0)); }));
+            CHECK(!(forward_pair(x, tp, false).data == y.data));  // eval with the moved statistics
+        }
         // forward_full pairing {1,1,2,2}: shared pairs bit-identical (test_mapper.cpp:268-292)
         Tensor xa({1, 2, 4, 2500});
         for (double& e : xa.data) e = u(rng);
