@@ -269,6 +269,9 @@ pkv_status pkv_mapper_init_params(const int64_t* geom5, const int64_t* cfg12, ui
 #define PKV_MAPPER_FP16W2 4u /* weights split hi+lo fp16, activations fp16 (2 MMAs per product) */
 #define PKV_MAPPER_FP16X3F 5u /* FP16X3 except the FFN down-projection, whose GELU input is one fp16
                                  plane (2 MMAs there; its hidden activations are half the bytes) */
+#define PKV_MAPPER_FP16F8 6u /* FP16X3's two correction products as e4m3 MMAs (kind::f8f6f4, half the tensor
+                                time each) in the same accumulator, for the conv2 / QKV / FFN1 / FFN2 GEMMs
+                                (Wo and stage 3 stay FP16X3): 2 MMA-equivalents per product */
 
 /* Uploads a mapper (weights in the pkv_mapper_init_params layout, fp64) to the
  * device; prepares the B200 weight layouts (K-major fp16 planes, BN folded,

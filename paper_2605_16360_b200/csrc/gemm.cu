@@ -3,6 +3,8 @@
 //   warp 1 : MMA issuer (one elected lane)
 //   warp 2 : TMEM allocator
 //   warps 4-7 : epilogue (thread = accumulator row; TMEM lane quadrant = warp % 4)
+#include <cuda_fp8.h>
+
 #include "gemm.cuh"
 
 namespace pkv {
@@ -62,7 +64,7 @@ __device__ __forceinline__ void epilogue_row(const GemmEpiParams& p, int64_t row
     const bool full = col0 + 32 <= N;
     float v[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.acc_scale;
     if ((EPI == EPI_F32 || EPI == EPI_GELU_PE) && p.row_scale) {
         const float rs = __ldg(p.row_scale + row);
 #pragma unroll
@@ -163,7 +165,9 @@ __device__ __forceinline__ void epilogue_row(const GemmEpiParams& p, int64_t row
     }
 }
 
-template <int EPI>
+// kF8Out: the e4m3 output planes (p.out_l8 / out_h8) are compiled in only for
+// the FP16F8 kernels (their register cost would spill the FP16X3 GELU epilogue)
+template <int EPI, bool kF8Out = false>
 __device__ __forceinline__ void epilogue_coalesced(const GemmEpiParams& p, int64_t row0, int64_t col0, int64_t M,
                                                    int64_t N, const uint32_t (&r)[32], float* stg) {
     const int lane = threadIdx.x & 31;
@@ -172,8 +176,9 @@ __device__ __forceinline__ void epilogue_coalesced(const GemmEpiParams& p, int64
         epilogue_row<EPI>(p, row0 + lane, col0, M, N, r, none);
         return;
     }
+    const float as = p.acc_scale;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) stg[lane * kStageLd + j] = __uint_as_float(r[j]);
+    for (int j = 0; j < 32; ++j) stg[lane * kStageLd + j] = __uint_as_float(r[j]) * as;
     __syncwarp();
     // warp-uniform fast path: the whole 32x32 chunk is in bounds (no per-row
     // checks, fully unrolled so independent rows overlap)
@@ -200,7 +205,15 @@ __device__ __forceinline__ void epilogue_coalesced(const GemmEpiParams& p, int64
                 const __half2 hi = __floats2half2_rn(x0, x1);
                 const float2 hb = __half22float2(hi);
                 *reinterpret_cast<__half2*>(oh + (rr >> 1) * step) = hi;
-                if (ol) *reinterpret_cast<__half2*>(ol + (rr >> 1) * step) = __floats2half2_rn(x0 - hb.x, x1 - hb.y);
+                if (kF8Out && p.out_l8) {
+                    const int64_t o8 = (row0 + rr + half) * p.ldo + col;
+                    *reinterpret_cast<__nv_fp8x2_storage_t*>(p.out_l8 + o8) = __nv_cvt_float2_to_fp8x2(
+                        make_float2((x0 - hb.x) * p.l8_mul, (x1 - hb.y) * p.l8_mul), __NV_SATFINITE, __NV_E4M3);
+                    *reinterpret_cast<__nv_fp8x2_storage_t*>(p.out_h8 + o8) = __nv_cvt_float2_to_fp8x2(
+                        make_float2(hb.x * p.h8_mul, hb.y * p.h8_mul), __NV_SATFINITE, __NV_E4M3);
+                } else if (ol) {
+                    *reinterpret_cast<__half2*>(ol + (rr >> 1) * step) = __floats2half2_rn(x0 - hb.x, x1 - hb.y);
+                }
             }
         } else {
 #pragma unroll 4
@@ -218,10 +231,22 @@ __device__ __forceinline__ void epilogue_coalesced(const GemmEpiParams& p, int64
                 const int64_t o = row * p.ldo + col;
                 if (c1ok) {
                     *reinterpret_cast<__half2*>(p.out_h + o) = hi;
-                    if (p.out_l) *reinterpret_cast<__half2*>(p.out_l + o) = __floats2half2_rn(x0 - hb.x, x1 - hb.y);
+                    if (kF8Out && p.out_l8) {
+                        *reinterpret_cast<__nv_fp8x2_storage_t*>(p.out_l8 + o) = __nv_cvt_float2_to_fp8x2(
+                            make_float2((x0 - hb.x) * p.l8_mul, (x1 - hb.y) * p.l8_mul), __NV_SATFINITE, __NV_E4M3);
+                        *reinterpret_cast<__nv_fp8x2_storage_t*>(p.out_h8 + o) = __nv_cvt_float2_to_fp8x2(
+                            make_float2(hb.x * p.h8_mul, hb.y * p.h8_mul), __NV_SATFINITE, __NV_E4M3);
+                    } else if (p.out_l) {
+                        *reinterpret_cast<__half2*>(p.out_l + o) = __floats2half2_rn(x0 - hb.x, x1 - hb.y);
+                    }
                 } else if (c0ok) {
                     p.out_h[o] = __low2half(hi);
-                    if (p.out_l) p.out_l[o] = __float2half_rn(x0 - hb.x);
+                    if (kF8Out && p.out_l8) {
+                        p.out_l8[o] = __nv_cvt_float_to_fp8((x0 - hb.x) * p.l8_mul, __NV_SATFINITE, __NV_E4M3);
+                        p.out_h8[o] = __nv_cvt_float_to_fp8(hb.x * p.h8_mul, __NV_SATFINITE, __NV_E4M3);
+                    } else if (p.out_l) {
+                        p.out_l[o] = __float2half_rn(x0 - hb.x);
+                    }
                 }
             }
         }
@@ -294,8 +319,9 @@ __device__ __forceinline__ void epilogue_resid_pref(const GemmEpiParams& p, int6
                                                     int64_t N, const uint32_t (&r)[32], const float (&res)[32],
                                                     float* stg) {
     const int lane = threadIdx.x & 31;
+    const float as = p.acc_scale;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) stg[lane * kStageLd + j] = __uint_as_float(r[j]);
+    for (int j = 0; j < 32; ++j) stg[lane * kStageLd + j] = __uint_as_float(r[j]) * as;
     __syncwarp();
     const int64_t col = col0 + lane;
     const bool cok = col < N;
@@ -514,11 +540,15 @@ void dispatch_planes(const GemmArgs& g, int sm, cudaStream_t st) {
 // columns each) for the GELU + hi/lo-split FFN1 epilogue, whose per-tile work
 // bounds that GEMM; 8 elsewhere (the residual path needs the registers and the
 // 3-deep operand ring that the larger staging buffer would cost)
-__host__ __device__ constexpr int epi_groups2(int epi) { return epi == EPI_GELU_F16X ? 4 : 2; }
+// FP16F8 halves the correction MMAs' tensor time, so its QKV (F16X) epilogue gets
+// 16 warps too (measured: QKV 12 % faster in mode 6, no gain in mode 3)
+__host__ __device__ constexpr int epi_groups2(int epi, bool f8) {
+    return (epi == EPI_GELU_F16X || (f8 && epi == EPI_F16X)) ? 4 : 2;
+}
 
-template <int NA, int NB, int EPI>
+template <int NA, int NB, int EPI, bool F8 = false>
 struct Cfg2 {
-    static constexpr int kEpiGroups2 = epi_groups2(EPI);
+    static constexpr int kEpiGroups2 = epi_groups2(EPI, F8);
     static constexpr int kThreads2 = 128 + 128 * kEpiGroups2;
     static constexpr int kStageBufBytes2 = 4 * kEpiGroups2 * 32 * kStageLd * 4;
     static constexpr int kHalf = 128 * kBK * 2;  // 16 KB: one operand half-tile plane
@@ -529,12 +559,18 @@ struct Cfg2 {
     static constexpr int kSmem = 1024 + kStages * kStageBytes + 256 + kStageBufBytes2;
 };
 
-template <int NA, int NB, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<NA, NB, EPI>::kThreads2, 1)
+// F8 (FP16F8, NA = NB = 2): each stage holds [A16 16 KB | A8lo 8 KB | A8hi 8 KB |
+// B16 16 KB | B8hi 8 KB | B8lo 8 KB] per CTA (the same 64 KB as FP16X3); per
+// 64-wide K block: 4 fp16 MMAs A16·B16 + 2 e4m3 MMAs A8lo·B8hi + 2 A8hi·B8lo
+// (tA1 / tA2 = A8lo / A8hi maps, tB1 / tB2 = B8hi / B8lo, SWIZZLE_64B).
+template <int NA, int NB, int EPI, bool F8 = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<NA, NB, EPI, F8>::kThreads2, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tA0, const __grid_constant__ CUtensorMap tA1,
-                 const __grid_constant__ CUtensorMap tB0, const __grid_constant__ CUtensorMap tB1, GemmEpiParams p,
+                 const __grid_constant__ CUtensorMap tB0, const __grid_constant__ CUtensorMap tB1,
+                 const __grid_constant__ CUtensorMap tA2, const __grid_constant__ CUtensorMap tB2, GemmEpiParams p,
                  int64_t M, int64_t N, int64_t K) {
-    using C = Cfg2<NA, NB, EPI>;
+    static_assert(!F8 || (NA == 2 && NB == 2), "FP16F8 uses the two-plane stage layout");
+    using C = Cfg2<NA, NB, EPI, F8>;
     constexpr int kEpiGroups2 = C::kEpiGroups2;
     constexpr int BN = 256;
     extern __shared__ uint8_t smem_raw[];
@@ -560,6 +596,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<NA, NB, EPI>::k
         tma_prefetch(&tB0);
         if (NA > 1) tma_prefetch(&tA1);
         if (NB > 1) tma_prefetch(&tB1);
+        if (F8) {
+            tma_prefetch(&tA2);
+            tma_prefetch(&tB2);
+        }
         for (int s = 0; s < C::kStages; ++s) {
             mbar_init(&full[s], 1);   // leader: arrive.expect_tx(both halves); bytes of both CTAs land here
             mbar_init(&empty[s], 1);  // multicast commit from the leader's MMA
@@ -588,9 +628,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<NA, NB, EPI>::k
                     uint8_t* st = smem + stage * C::kStageBytes;
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
                     tma_load_2d_2sm(st, &tA0, &full[stage], kb * kBK, m0);
-                    if (NA > 1) tma_load_2d_2sm(st + C::kHalf, &tA1, &full[stage], kb * kBK, m0);
-                    tma_load_2d_2sm(st + NA * C::kHalf, &tB0, &full[stage], kb * kBK, n0);
-                    if (NB > 1) tma_load_2d_2sm(st + (NA + 1) * C::kHalf, &tB1, &full[stage], kb * kBK, n0);
+                    if (F8) {
+                        tma_load_2d_2sm(st + C::kHalf, &tA1, &full[stage], kb * kBK, m0);
+                        tma_load_2d_2sm(st + C::kHalf + C::kHalf / 2, &tA2, &full[stage], kb * kBK, m0);
+                        tma_load_2d_2sm(st + 2 * C::kHalf, &tB0, &full[stage], kb * kBK, n0);
+                        tma_load_2d_2sm(st + 3 * C::kHalf, &tB1, &full[stage], kb * kBK, n0);
+                        tma_load_2d_2sm(st + 3 * C::kHalf + C::kHalf / 2, &tB2, &full[stage], kb * kBK, n0);
+                    } else {
+                        if (NA > 1) tma_load_2d_2sm(st + C::kHalf, &tA1, &full[stage], kb * kBK, m0);
+                        tma_load_2d_2sm(st + NA * C::kHalf, &tB0, &full[stage], kb * kBK, n0);
+                        if (NB > 1) tma_load_2d_2sm(st + (NA + 1) * C::kHalf, &tB1, &full[stage], kb * kBK, n0);
+                    }
                     if (++stage == C::kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -614,16 +662,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<NA, NB, EPI>::k
                     tc_fence_after();
                     if (elect_one()) {
                         uint8_t* st = smem + stage * C::kStageBytes;
-                        const uint64_t a0 = desc_sw128(st);
-                        const uint64_t a1 = desc_sw128(st + C::kHalf);
-                        const uint64_t b0 = desc_sw128(st + NA * C::kHalf);
-                        const uint64_t b1 = desc_sw128(st + (NA + 1) * C::kHalf);
+                        if (F8) {
+                            const uint64_t a0 = desc_sw128(st), b0 = desc_sw128(st + 2 * C::kHalf);
+                            const uint64_t a8l = desc_sw64(st + C::kHalf);
+                            const uint64_t a8h = desc_sw64(st + C::kHalf + C::kHalf / 2);
+                            const uint64_t b8h = desc_sw64(st + 3 * C::kHalf);
+                            const uint64_t b8l = desc_sw64(st + 3 * C::kHalf + C::kHalf / 2);
 #pragma unroll
-                        for (int kk = 0; kk < kBK / 16; ++kk) {
-                            const uint64_t off = (uint64_t)(kk * 2);
-                            mma_f16_ss_2sm(d, a0 + off, b0 + off, idesc, (kb | kk) != 0);
-                            if (NA > 1) mma_f16_ss_2sm(d, a1 + off, b0 + off, idesc, 1);
-                            if (NB > 1) mma_f16_ss_2sm(d, a0 + off, b1 + off, idesc, 1);
+                            for (int kk = 0; kk < kBK / 16; ++kk)
+                                mma_f16_ss_2sm(d, a0 + kk * 2, b0 + kk * 2, idesc, (kb | kk) != 0);
+#pragma unroll
+                            for (int kk = 0; kk < kBK / 32; ++kk) {  // e4m3: K = 32 (32 B) per MMA
+                                mma_f8_ss_2sm(d, a8l + kk * 2, b8h + kk * 2, idesc, 1);
+                                mma_f8_ss_2sm(d, a8h + kk * 2, b8l + kk * 2, idesc, 1);
+                            }
+                        } else {
+                            const uint64_t a0 = desc_sw128(st);
+                            const uint64_t a1 = desc_sw128(st + C::kHalf);
+                            const uint64_t b0 = desc_sw128(st + NA * C::kHalf);
+                            const uint64_t b1 = desc_sw128(st + (NA + 1) * C::kHalf);
+#pragma unroll
+                            for (int kk = 0; kk < kBK / 16; ++kk) {
+                                const uint64_t off = (uint64_t)(kk * 2);
+                                mma_f16_ss_2sm(d, a0 + off, b0 + off, idesc, (kb | kk) != 0);
+                                if (NA > 1) mma_f16_ss_2sm(d, a1 + off, b0 + off, idesc, 1);
+                                if (NB > 1) mma_f16_ss_2sm(d, a0 + off, b1 + off, idesc, 1);
+                            }
                         }
                         mma_commit_2sm(&empty[stage], 0x3);
                     }
@@ -690,11 +754,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<NA, NB, EPI>::k
 #pragma unroll 1
             for (int c0 = cbeg; c0 < cend; c0 += 64) {
                 if (c0 + 32 < cend) tmem_ld32(taddr + c0 + 32, r[1]);
-                if (n0 + c0 < N) epilogue_coalesced<EPI>(p, row - lane, n0 + c0, M, N, r[0], stagebuf);
+                if (n0 + c0 < N) epilogue_coalesced<EPI, F8>(p, row - lane, n0 + c0, M, N, r[0], stagebuf);
                 tmem_ld_wait();
                 if (c0 + 32 < cend) {
                     if (c0 + 64 < cend) tmem_ld32(taddr + c0 + 64, r[0]);
-                    if (n0 + c0 + 32 < N) epilogue_coalesced<EPI>(p, row - lane, n0 + c0 + 32, M, N, r[1], stagebuf);
+                    if (n0 + c0 + 32 < N) epilogue_coalesced<EPI, F8>(p, row - lane, n0 + c0 + 32, M, N, r[1], stagebuf);
                     tmem_ld_wait();
                 }
             }
@@ -715,22 +779,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<NA, NB, EPI>::k
     }
 }
 
-template <int NA, int NB, int EPI>
+template <int NA, int NB, int EPI, bool F8 = false>
 void launch2(const GemmArgs& g, int sm_count, cudaStream_t st) {
-    using C = Cfg2<NA, NB, EPI>;
-    auto kern = gemm2_kernel<NA, NB, EPI>;
+    using C = Cfg2<NA, NB, EPI, F8>;
+    auto kern = gemm2_kernel<NA, NB, EPI, F8>;
     static std::atomic<uint64_t> attr_set{0};
     if (first_on_device(attr_set)) PKV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     // B re-encoded with 128-row boxes (each CTA of the pair loads half of the N tile)
     CUtensorMap b[2];
-    for (int q = 0; q < NB; ++q) {
+    for (int q = 0; q < (F8 ? 1 : NB); ++q) {
         b[q] = make_tmap_2d(g.b_ptr[q], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, (uint64_t)g.K, (uint64_t)g.N,
                             (uint64_t)g.ldb * 2, kBK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
     }
     if (NB == 1) b[1] = b[0];
+    CUtensorMap a2 = g.a[0], b2 = b[0];
+    if (F8) {  // B planes: [0] fp16 hi, then e4m3 hi / lo (64-B rows, 128-row boxes)
+        b[1] = make_tmap_2d(g.b8[0], CU_TENSOR_MAP_DATA_TYPE_UINT8, (uint64_t)g.K, (uint64_t)g.N, (uint64_t)g.K, kBK,
+                            128, CU_TENSOR_MAP_SWIZZLE_64B);
+        b2 = make_tmap_2d(g.b8[1], CU_TENSOR_MAP_DATA_TYPE_UINT8, (uint64_t)g.K, (uint64_t)g.N, (uint64_t)g.K, kBK, 128,
+                          CU_TENSOR_MAP_SWIZZLE_64B);
+        a2 = g.a8h;
+    }
     const int64_t tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256);
     int64_t clusters = tiles < sm_count / 2 ? tiles : sm_count / 2;
-    kern<<<(unsigned)(2 * clusters), C::kThreads2, C::kSmem, st>>>(g.a[0], g.a[1], b[0], b[1], g.p, g.M, g.N, g.K);
+    kern<<<(unsigned)(2 * clusters), C::kThreads2, C::kSmem, st>>>(g.a[0], g.a[1], b[0], b[1], a2, b2, g.p, g.M, g.N,
+                                                                   g.K);
     check_launch("gemm2_kernel");
 }
 
@@ -746,6 +819,15 @@ void dispatch2_epi(const GemmArgs& g, int sm, cudaStream_t st) {
 }
 
 void dispatch2(const GemmArgs& g, int sm, cudaStream_t st) {
+    if (g.f8) {
+        switch (g.epi) {
+            case EPI_F16X: return launch2<2, 2, EPI_F16X, true>(g, sm, st);
+            case EPI_GELU_F16X: return launch2<2, 2, EPI_GELU_F16X, true>(g, sm, st);
+            case EPI_RESID: return launch2<2, 2, EPI_RESID, true>(g, sm, st);
+            case EPI_GELU_PE: return launch2<2, 2, EPI_GELU_PE, true>(g, sm, st);
+            default: throw Error{PKV_ECONFIG, "FP16F8 GEMM: unsupported epilogue"};
+        }
+    }
     if (g.na == 1 && g.nb == 1) return dispatch2_epi<1, 1>(g, sm, st);
     if (g.na == 2 && g.nb == 1) return dispatch2_epi<2, 1>(g, sm, st);
     if (g.na == 1 && g.nb == 2) return dispatch2_epi<1, 2>(g, sm, st);
@@ -773,8 +855,24 @@ void gemm_set_b(GemmArgs& g, int plane, const __half* b, int64_t N, int64_t K, i
     g.ldb = ldb;
 }
 
+void gemm_set_a8(GemmArgs& g, const uint8_t* lo8, const uint8_t* hi8, int64_t M, int64_t K, int64_t lda) {
+    g.a[1] = make_tmap_2d(lo8, CU_TENSOR_MAP_DATA_TYPE_UINT8, (uint64_t)K, (uint64_t)M, (uint64_t)lda, kBK, kBM,
+                          CU_TENSOR_MAP_SWIZZLE_64B);
+    g.a8h = make_tmap_2d(hi8, CU_TENSOR_MAP_DATA_TYPE_UINT8, (uint64_t)K, (uint64_t)M, (uint64_t)lda, kBK, kBM,
+                         CU_TENSOR_MAP_SWIZZLE_64B);
+    g.na = 2;
+    g.f8 = true;
+}
+
+void gemm_set_b8(GemmArgs& g, const uint8_t* hi8, const uint8_t* lo8) {
+    g.b8[0] = hi8;
+    g.b8[1] = lo8;
+    g.nb = 2;
+}
+
 void gemm_run(const GemmArgs& g, int sm_count, cudaStream_t st) {
     if (g.M == 0 || g.N == 0) return;
+    PKV_REQUIRE(!g.f8 || g.pair, PKV_ECONFIG, "FP16F8 GEMMs run on the CTA-pair kernel (M, N >= 256)");
     if (g.pair) return dispatch2(g, sm_count, st);
     switch (g.bn) {
         case 256: return dispatch_planes<256>(g, sm_count, st);

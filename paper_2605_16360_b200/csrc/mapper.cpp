@@ -6,6 +6,8 @@
 //     the convs, Q_l and out_w folded into one stage-3 projection, fp64 math),
 //   - forward orchestration: all windows of all (deduplicated) proxy layers are
 //     batched into the GEMM M dimension, in bounded row chunks.
+#include <cuda_fp8.h>
+
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -273,14 +275,47 @@ WeightPlanes Mapper::upload_planes(const std::vector<double>& W, int64_t N, int6
     return p;
 }
 
+// FP16F8: W' = W·2^w with max |W'| in [2^(w_top−1), 2^w_top) (fp16 hi plane),
+// e4m3 planes of W'_hi / lo_mul and (W' − W'_hi) / hi_mul (gemm.cuh).
+WeightPlanes Mapper::upload_planes_f8(const std::vector<double>& W, int64_t N, int64_t K, const F8Class& cls) {
+    if (!f8) return upload_planes(W, N, K);
+    double mx = 0.0;
+    for (double v : W) mx = std::max(mx, std::fabs(v));
+    int e = 0;
+    if (mx > 0.0) std::frexp(mx, &e);  // mx < 2^e
+    const int w = cls.w_top - e;
+    const double sc = std::ldexp(1.0, w);
+    std::vector<__half> hi(W.size()), lo(W.size());
+    std::vector<uint8_t> h8(W.size()), l8(W.size());
+    for (size_t i = 0; i < W.size(); ++i) {
+        const double v = W[i] * sc;
+        hi[i] = __double2half(v);
+        const double h = static_cast<double>(__half2float(hi[i]));
+        lo[i] = __double2half(v - h);  // the FP16X3 fallback for GEMMs too small for the pair kernel
+        h8[i] = __nv_cvt_float_to_fp8(static_cast<float>(h / cls.lo_mul), __NV_SATFINITE, __NV_E4M3);
+        l8[i] = __nv_cvt_float_to_fp8(static_cast<float>((v - h) / cls.hi_mul), __NV_SATFINITE, __NV_E4M3);
+    }
+    WeightPlanes p;
+    p.N = N;
+    p.K = K;
+    p.hi = upload(hi, owned);
+    p.lo = upload(lo, owned);
+    p.h8 = upload(h8, owned);
+    p.l8 = upload(l8, owned);
+    p.acc_scale = static_cast<float>(std::ldexp(1.0, -w));
+    p.cls = cls;
+    return p;
+}
+
 Mapper::Mapper(pkv_ctx c, const Geometry& g, const Config& cf, const double* blob, int64_t count, uint32_t precision)
     : ctx(c), geom(g), cfg(cf) {
     geom.validate();
     cfg.validate();
-    PKV_REQUIRE(precision >= 1 && precision <= 5, PKV_ECONFIG, "unknown mapper precision mode ", precision);
-    na = (precision == 2 || precision == 3 || precision == 5) ? 2 : 1;
-    nb = (precision == 3 || precision == 4 || precision == 5) ? 2 : 1;
+    PKV_REQUIRE(precision >= 1 && precision <= 6, PKV_ECONFIG, "unknown mapper precision mode ", precision);
+    na = (precision == 2 || precision == 3 || precision == 5 || precision == 6) ? 2 : 1;
+    nb = (precision == 3 || precision == 4 || precision == 5 || precision == 6) ? 2 : 1;
     ffn2_single_act = precision == 5;
+    f8 = precision == 6 && use_pair;
     const int64_t D = cfg.d_time;
     PKV_REQUIRE(D % 128 == 0 && D <= 1024, PKV_ECONFIG, "GPU mapper needs d_time % 128 == 0 and <= 1024, got ", D);
     if (cfg.enc_active && cfg.encoder_layers > 0) {
@@ -348,7 +383,7 @@ Mapper::Mapper(pkv_ctx c, const Geometry& g, const Config& cf, const double* blo
             }
             b2f[co] = b2[co] * s2[co] + t2[co];
         }
-        conv2 = upload_planes(w2r, D, 3 * mid);
+        conv2 = upload_planes_f8(w2r, D, 3 * mid, kF8Row);
         conv2_b = upload(to_f32(b2f), owned);
     } else {
         bypass_w = upload(to_f32(P["stem.bypass.w"]), owned);  // [D, hs, 1] == [D][hs]
@@ -373,13 +408,13 @@ Mapper::Mapper(pkv_ctx c, const Geometry& g, const Config& cf, const double* blo
                 const auto& bb = P[p + "attn.b" + m];
                 bqkv.insert(bqkv.end(), bb.begin(), bb.end());
             }
-            b.qkv = upload_planes(wqkv, 3 * D, D);
+            b.qkv = upload_planes_f8(wqkv, 3 * D, D, kF8Act);
             b.qkv_b = upload(to_f32(bqkv), owned);
             b.o = upload_planes(transpose(P[p + "attn.wo"], D, D), D, D);
             b.o_b = upload(to_f32(P[p + "attn.bo"]), owned);
-            b.f1 = upload_planes(transpose(P[p + "ffn1.w"], D, F), F, D);
+            b.f1 = upload_planes_f8(transpose(P[p + "ffn1.w"], D, F), F, D, kF8Act);
             b.f1_b = upload(to_f32(P[p + "ffn1.b"]), owned);
-            b.f2 = upload_planes(transpose(P[p + "ffn2.w"], F, D), D, F);
+            b.f2 = upload_planes_f8(transpose(P[p + "ffn2.w"], F, D), D, F, kF8Act);
             b.f2_b = upload(to_f32(P[p + "ffn2.b"]), owned);
             b.ln1_g = upload(to_f32(P[p + "ln1.gamma"]), owned);
             b.ln1_b = upload(to_f32(P[p + "ln1.beta"]), owned);
@@ -448,6 +483,19 @@ void Mapper::gemm(const __half* a_h, const __half* a_l, int64_t M, const WeightP
     g.bn = pick_bn(w.N);
     g.pair = use_pair && w.N >= 256 && M >= 256;  // cta_group::2 256x256 tiles for the big projections
     g.epi = epi;
+    p.acc_scale *= w.acc_scale;
+    if (f8_gemm(w, M)) {  // FP16F8: a_l holds the e4m3 lo plane then the hi plane ([M, K] bytes each)
+        gemm_set_a(g, 0, a_h, M, w.K, w.K);
+        const auto* l8 = reinterpret_cast<const uint8_t*>(a_l);
+        gemm_set_a8(g, l8, l8 + M * w.K, M, w.K, w.K);
+        gemm_set_b(g, 0, w.hi, w.N, w.K, w.K);
+        gemm_set_b8(g, w.h8, w.l8);
+        p.bias = bias;
+        g.p = p;
+        gemm_run(g, ctx->sm_count, st);
+        count_launch(ctx);
+        return;
+    }
     gemm_set_a(g, 0, a_h, M, w.K, w.K);
     g.a[1] = g.a[0];
     g.na = 1;
@@ -460,6 +508,18 @@ void Mapper::gemm(const __half* a_h, const __half* a_l, int64_t M, const WeightP
     g.p = p;
     gemm_run(g, ctx->sm_count, st);
     count_launch(ctx);
+}
+
+// The e4m3 planes the producer of an FP16F8 GEMM's A operand writes into the
+// fp16 lo plane's buffer (lo8 then hi8, `elems` bytes each); empty otherwise.
+F8Out Mapper::f8_planes(const WeightPlanes& w, int64_t M, __half* lo_buf, int64_t elems) const {
+    F8Out o;
+    if (!f8_gemm(w, M) || !lo_buf) return o;
+    o.lo8 = reinterpret_cast<uint8_t*>(lo_buf);
+    o.hi8 = o.lo8 + elems;
+    o.lo_mul = w.cls.lo_mul;
+    o.hi_mul = w.cls.hi_mul;
+    return o;
 }
 
 // x: caller's scores; unit_off[u]: element offset of unit u's [H_s, N] slab
@@ -532,7 +592,8 @@ void Mapper::run(const float* x, const std::vector<int64_t>& unit_off, int64_t N
         if (cfg.conv_active) {
             __half* col_h = reinterpret_cast<__half*>(arena);
             __half* col_l = na > 1 ? col_h + rows * 3 * mid : nullptr;
-            launch_conv1_im2col(src, mean, conv1_w, conv1_b, static_cast<int>(mid), col_h, col_l, rscale, st);
+            launch_conv1_im2col(src, mean, conv1_w, conv1_b, static_cast<int>(mid), col_h, col_l, rscale, st,
+                                f8_planes(conv2, rows, col_l, rows * 3 * mid));
             count_launch(ctx);
             GemmEpiParams p;
             p.out_f32 = z;
@@ -555,7 +616,8 @@ void Mapper::run(const float* x, const std::vector<int64_t>& unit_off, int64_t N
             __half* f_h = h_h + rows * D * act_planes;  // ffn phase reuses qkv/ctx space
             __half* f_l = na > 1 ? f_h + rows * F : nullptr;
             for (const Block& b : blocks) {
-                launch_layernorm(z, rows, static_cast<int>(D), b.ln1_g, b.ln1_b, h_h, h_l, st);
+                launch_layernorm(z, rows, static_cast<int>(D), b.ln1_g, b.ln1_b, h_h, h_l, st,
+                                 f8_planes(b.qkv, rows, h_l, rows * D));
                 count_launch(ctx);
                 GemmEpiParams pq;
                 pq.out_h = qkv;
@@ -568,12 +630,21 @@ void Mapper::run(const float* x, const std::vector<int64_t>& unit_off, int64_t N
                 po.out_f32 = z;
                 po.ldo = D;
                 gemm(c_h, c_l, rows, b.o, b.o_b, EPI_RESID, po, st);
-                launch_layernorm(z, rows, static_cast<int>(D), b.ln2_g, b.ln2_b, h_h, h_l, st);
+                launch_layernorm(z, rows, static_cast<int>(D), b.ln2_g, b.ln2_b, h_h, h_l, st,
+                                 f8_planes(b.f1, rows, h_l, rows * D));
                 count_launch(ctx);
                 GemmEpiParams pf;
                 pf.out_h = f_h;
                 pf.out_l = ffn2_single_act ? nullptr : f_l;  // mode 5: FFN2 reads one activation plane
                 pf.ldo = F;
+                if (f8_gemm(b.f2, rows)) {  // mode 6: FFN2's e4m3 correction planes
+                    const F8Out o = f8_planes(b.f2, rows, f_l, rows * F);
+                    pf.out_l = nullptr;
+                    pf.out_l8 = o.lo8;
+                    pf.out_h8 = o.hi8;
+                    pf.l8_mul = o.lo_mul;
+                    pf.h8_mul = o.hi_mul;
+                }
                 gemm(h_h, h_l, rows, b.f1, b.f1_b, EPI_GELU_F16X, pf, st);
                 GemmEpiParams p2;
                 p2.out_f32 = z;

@@ -10,6 +10,7 @@
 
 #include "gemm.cuh"
 #include "internal.h"
+#include "mapper_kernels.cuh"
 
 namespace pkv {
 
@@ -40,6 +41,11 @@ struct WeightPlanes {
     __half* hi = nullptr;
     __half* lo = nullptr;
     int64_t N = 0, K = 0;  // B operand [N, K], K-major
+    // FP16F8 (precision 6): hi = fp16(W·2^w), e4m3 planes h8 = hi / lo_mul, l8 = (W·2^w − hi) / hi_mul
+    uint8_t* h8 = nullptr;
+    uint8_t* l8 = nullptr;
+    float acc_scale = 1.0f;  // 2^-w
+    F8Class cls{};
 };
 
 struct Block {
@@ -61,6 +67,7 @@ public:
     Config cfg;
     int na = 2, nb = 1;
     bool ffn2_single_act = false;  // precision mode 5
+    bool f8 = false;               // precision mode 6 (FP16F8)
     int64_t rows_cap = int64_t(1) << 20;  // rows per chunk (bounds the workspace)
     bool use_pair = getenv("PKV_NO_PAIR") == nullptr;  // CTA-pair GEMMs (tuning/AB switch)
     // QKV projection with one fp16 MMA (its output is rounded to one fp16 plane
@@ -70,6 +77,12 @@ public:
 
 private:
     WeightPlanes upload_planes(const std::vector<double>& W, int64_t N, int64_t K);
+    // FP16F8 weights whose GEMM at M rows runs on the pair kernel: the producer of
+    // its A operand then writes the e4m3 planes instead of the fp16 lo plane
+    bool f8_gemm(const WeightPlanes& w, int64_t M) const { return w.h8 && use_pair && w.N >= 256 && M >= 256; }
+    F8Out f8_planes(const WeightPlanes& w, int64_t M, __half* lo_buf, int64_t elems) const;
+    // FP16F8 planes when precision 6 (else upload_planes)
+    WeightPlanes upload_planes_f8(const std::vector<double>& W, int64_t N, int64_t K, const F8Class& cls);
     void gemm(const __half* a_h, const __half* a_l, int64_t M, const WeightPlanes& w, const float* bias, GemmEpi epi,
               GemmEpiParams p, cudaStream_t st, bool single = false, bool a_single = false);
 

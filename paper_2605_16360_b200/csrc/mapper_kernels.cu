@@ -12,11 +12,17 @@
 //                       softmaxes over the synthetic heads and the value·out_w
 //                       dot (mapper.cpp:321-341)
 //   window_average_kernel sliding_forward's overlap average (mapper.cpp:356-375)
+#include <cuda_fp8.h>
+
 #include "mapper_kernels.cuh"
 #include "sm100.cuh"
 
 namespace pkv {
 namespace {
+
+__device__ __forceinline__ uint32_t e4m3x2(float a, float b) {
+    return (uint32_t)__nv_cvt_float2_to_fp8x2(make_float2(a, b), __NV_SATFINITE, __NV_E4M3);
+}
 
 // Power of two s with max_abs·s in [2^13, 2^14) (1 for an all-zero row); the
 // GEMM epilogue multiplies by 1/s (GemmEpiParams::row_scale). Exact: scaling by
@@ -72,7 +78,7 @@ constexpr int kConvTok = 64;  // tokens per block (amortises the per-block weigh
 // full 22-bit precision this way.
 __global__ void conv1_im2col_kernel(WinSrc src, const float* __restrict__ inv_mean, const float* __restrict__ w1,
                                     const float* __restrict__ b1, int mid, __half* __restrict__ col_h,
-                                    __half* __restrict__ col_l, float* __restrict__ rinv) {
+                                    __half* __restrict__ col_l, float* __restrict__ rinv, F8Out f8) {
     extern __shared__ float sm[];
     const int hs = src.hs, kw = hs * 3, kws = kw + 1;
     float* sw = sm;                            // [mid][kws]
@@ -145,7 +151,21 @@ __global__ void conv1_im2col_kernel(WinSrc src, const float* __restrict__ inv_me
         }
         const int64_t off = ((int64_t)uw * src.Lw + t0 + tt) * K + col;
         *reinterpret_cast<uint4*>(col_h + off) = *reinterpret_cast<const uint4*>(hi);
-        if (col_l) *reinterpret_cast<uint4*>(col_l + off) = *reinterpret_cast<const uint4*>(lo);
+        if (f8.lo8) {  // lo[e] holds v − hi exactly enough (fp16 of the residual) for an e4m3 rounding
+            uint32_t l8[2], h8[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int e = 4 * q;
+                l8[q] = e4m3x2(__half2float(lo[e]) * f8.lo_mul, __half2float(lo[e + 1]) * f8.lo_mul) |
+                        (e4m3x2(__half2float(lo[e + 2]) * f8.lo_mul, __half2float(lo[e + 3]) * f8.lo_mul) << 16);
+                h8[q] = e4m3x2(__half2float(hi[e]) * f8.hi_mul, __half2float(hi[e + 1]) * f8.hi_mul) |
+                        (e4m3x2(__half2float(hi[e + 2]) * f8.hi_mul, __half2float(hi[e + 3]) * f8.hi_mul) << 16);
+            }
+            *reinterpret_cast<uint2*>(f8.lo8 + off) = make_uint2(l8[0], l8[1]);
+            *reinterpret_cast<uint2*>(f8.hi8 + off) = make_uint2(h8[0], h8[1]);
+        } else if (col_l) {
+            *reinterpret_cast<uint4*>(col_l + off) = *reinterpret_cast<const uint4*>(lo);
+        }
     }
 }
 
@@ -172,7 +192,8 @@ __global__ void bypass_stem_kernel(WinSrc src, const float* __restrict__ inv_mea
 // One warp per row of D = 128·V floats.
 template <int V>
 __global__ void layernorm_kernel(const float* __restrict__ z, int64_t rows, const float* __restrict__ g,
-                                 const float* __restrict__ b, __half* __restrict__ hi, __half* __restrict__ lo) {
+                                 const float* __restrict__ b, __half* __restrict__ hi, __half* __restrict__ lo,
+                                 F8Out f8) {
     constexpr int D = 128 * V;
     const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -203,14 +224,24 @@ __global__ void layernorm_kernel(const float* __restrict__ z, int64_t rows, cons
         const float x[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
         __align__(8) __half h4[4];
         __align__(8) __half l4[4];
+        float r4[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             const float y = g[c0 + t] * ((x[t] - mu) * inv) + b[c0 + t];
             h4[t] = __float2half_rn(y);
-            l4[t] = __float2half_rn(y - __half2float(h4[t]));
+            r4[t] = y - __half2float(h4[t]);
+            l4[t] = __float2half_rn(r4[t]);
         }
         *reinterpret_cast<uint2*>(hi + row * D + c0) = *reinterpret_cast<const uint2*>(h4);
-        if (lo) *reinterpret_cast<uint2*>(lo + row * D + c0) = *reinterpret_cast<const uint2*>(l4);
+        if (f8.lo8) {
+            *reinterpret_cast<uint32_t*>(f8.lo8 + row * D + c0) =
+                e4m3x2(r4[0] * f8.lo_mul, r4[1] * f8.lo_mul) | (e4m3x2(r4[2] * f8.lo_mul, r4[3] * f8.lo_mul) << 16);
+            *reinterpret_cast<uint32_t*>(f8.hi8 + row * D + c0) =
+                e4m3x2(__half2float(h4[0]) * f8.hi_mul, __half2float(h4[1]) * f8.hi_mul) |
+                (e4m3x2(__half2float(h4[2]) * f8.hi_mul, __half2float(h4[3]) * f8.hi_mul) << 16);
+        } else if (lo) {
+            *reinterpret_cast<uint2*>(lo + row * D + c0) = *reinterpret_cast<const uint2*>(l4);
+        }
     }
 }
 
@@ -342,7 +373,7 @@ void launch_window_mean(const MapperSrc& s, float* mean_out, cudaStream_t st) {
 }
 
 void launch_conv1_im2col(const MapperSrc& s, const float* inv_mean, const float* w1, const float* b1, int mid,
-                         __half* col_h, __half* col_l, float* rinv, cudaStream_t st) {
+                         __half* col_h, __half* col_l, float* rinv, cudaStream_t st, F8Out f8) {
     WinSrc w{s.x, s.unit_off, s.win_off, s.head_stride, s.W, s.Lw, s.hs};
     const size_t smem = sizeof(float) * ((size_t)mid * (s.hs * 3 + 1) + (size_t)s.hs * (kConvTok + 4) +
                                          (size_t)(kConvTok + 2) * mid + (kConvTok + 2) + kConvTok);
@@ -354,7 +385,7 @@ void launch_conv1_im2col(const MapperSrc& s, const float* inv_mean, const float*
         attr[dev & 63] = smem;
     }
     const dim3 grid((unsigned)((s.Lw + kConvTok - 1) / kConvTok), (unsigned)(s.units * s.W));
-    conv1_im2col_kernel<<<grid, 256, smem, st>>>(w, inv_mean, w1, b1, mid, col_h, col_l, rinv);
+    conv1_im2col_kernel<<<grid, 256, smem, st>>>(w, inv_mean, w1, b1, mid, col_h, col_l, rinv, f8);
     check_launch("conv1_im2col_kernel");
 }
 
@@ -367,13 +398,13 @@ void launch_bypass_stem(const MapperSrc& s, const float* inv_mean, const float* 
 }
 
 void launch_layernorm(const float* z, int64_t rows, int D, const float* g, const float* b, __half* hi, __half* lo,
-                      cudaStream_t st) {
+                      cudaStream_t st, F8Out f8) {
     const unsigned blocks = (unsigned)((rows + 7) / 8);
     switch (D) {
-        case 128: layernorm_kernel<1><<<blocks, 256, 0, st>>>(z, rows, g, b, hi, lo); break;
-        case 256: layernorm_kernel<2><<<blocks, 256, 0, st>>>(z, rows, g, b, hi, lo); break;
-        case 512: layernorm_kernel<4><<<blocks, 256, 0, st>>>(z, rows, g, b, hi, lo); break;
-        case 1024: layernorm_kernel<8><<<blocks, 256, 0, st>>>(z, rows, g, b, hi, lo); break;
+        case 128: layernorm_kernel<1><<<blocks, 256, 0, st>>>(z, rows, g, b, hi, lo, f8); break;
+        case 256: layernorm_kernel<2><<<blocks, 256, 0, st>>>(z, rows, g, b, hi, lo, f8); break;
+        case 512: layernorm_kernel<4><<<blocks, 256, 0, st>>>(z, rows, g, b, hi, lo, f8); break;
+        case 1024: layernorm_kernel<8><<<blocks, 256, 0, st>>>(z, rows, g, b, hi, lo, f8); break;
         default: throw Error{PKV_ECONFIG, cat("GPU layernorm supports d_time in {128,256,512,1024}, got ", D)};
     }
     check_launch("layernorm_kernel");

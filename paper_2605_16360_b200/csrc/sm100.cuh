@@ -137,6 +137,16 @@ __device__ __forceinline__ void mma_f16_ss_2sm(uint32_t tmem_d, uint64_t adesc, 
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+__device__ __forceinline__ void mma_f8_ss_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 // Commit the pair's MMAs to the same-offset barrier in every CTA of `mask`.
 __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar, uint16_t mask) {
     asm volatile(
@@ -186,6 +196,20 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uin
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
         "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::f8f6f4 (e4m3 in with the same
+// instruction descriptor bits as kind::f16 / fp16, fp32 accumulate): K = 32 per
+// instruction. Accumulates into the same fp32 TMEM tile as kind::f16 MMAs
+// (tools/probe_f8mma.cu checks the mixed accumulation).
+__device__ __forceinline__ void mma_f8_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
 
@@ -452,6 +476,21 @@ __device__ __forceinline__ uint64_t desc_sw128(const void* smem_tile) {
     d |= (uint64_t)(1024 >> 4) << 32;       // SBO = 1024 B   [32,46)
     d |= 1ull << 46;                        // version = 1 (sm100)
     d |= 2ull << 61;                        // SWIZZLE_128B
+    return d;
+}
+
+// K-major e4m3 operand in the 64-byte-swizzle layout TMA
+// (CU_TENSOR_MAP_SWIZZLE_64B) writes for 64-element K blocks: rows of 64 B,
+// 8-row core groups 512 B apart (SBO), tile base 512-B aligned. The second
+// K = 32 half of a row is +32 B (+2 in the address field), as with SW128.
+__device__ __forceinline__ uint64_t desc_sw64(const void* smem_tile) {
+    const uint64_t addr = smem_u32(smem_tile);
+    uint64_t d = 0;
+    d |= (addr >> 4) & 0x3FFFull;
+    d |= 1ull << 16;
+    d |= (uint64_t)(512 >> 4) << 32;  // SBO = 512 B
+    d |= 1ull << 46;
+    d |= 4ull << 61;  // SWIZZLE_64B
     return d;
 }
 

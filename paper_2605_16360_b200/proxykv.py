@@ -28,7 +28,7 @@ __all__ = [
     "LossConfig", "LossReport", "loss_total", "MapperTrainer",
     "layer_pair", "window_offsets", "mapper_init_params", "ShapeError", "PkvValueError", "ConfigError",
     "CudaError", "NoDeviceError", "PkvError", "SCORE_REDUCE_MAX", "SCORE_REDUCE_SUM", "SCORE_CAUSAL",
-    "MAPPER_FP16", "MAPPER_FP16X2", "MAPPER_FP16X3", "SHARD_LAYER", "SHARD_HEAD", "ShardPlan", "shard_plan",
+    "MAPPER_FP16", "MAPPER_FP16X2", "MAPPER_FP16X3", "MAPPER_FP16F8", "SHARD_LAYER", "SHARD_HEAD", "ShardPlan", "shard_plan",
     "Comm", "shard_exchange_schedule", "write_trace", "read_trace", "write_checkpoint", "read_checkpoint", "IoError", "BadMagicError",
     "VersionMismatchError", "TruncatedFileError", "PayloadLengthError",
 ]
@@ -41,6 +41,7 @@ MAPPER_FP16X2 = 2
 MAPPER_FP16X3 = 3
 MAPPER_FP16W2 = 4
 MAPPER_FP16X3F = 5
+MAPPER_FP16F8 = 6
 SHARD_LAYER = 0
 SHARD_HEAD = 1
 COMM_ID_BYTES = 128
