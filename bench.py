@@ -418,7 +418,12 @@ def stage_breakdown(P, ctx, arm, c, stream, args):
     out["score_lse_ms"] = time_loop(lse_call, it, stream)
     out["score_pool_ms"] = time_loop(pool_call, it, stream)
     out["map_ms"] = time_loop(map_call, it, stream)
+    # the short stages: one untimed loop first — the first back-to-back loop after the
+    # long stages runs ~45 % slow for select (tools/probe_select_bench.py: 56.8 then
+    # 37.0 us on the same data; ncu: 39 us per launch)
+    time_loop(sel_call, 20, stream)
     out["select_ms"] = time_loop(sel_call, 20, stream)
+    time_loop(cmp_call, 10, stream)
     out["compact_ms"] = time_loop(cmp_call, 10, stream)
     # causal scoring with the LSE emitted by the proxy's own prefill
     # attention (its O is the proxy model's output anyway): one scoring pass
