@@ -132,3 +132,40 @@ def test_backward_accumulates_and_errors(gpu):
         tr.forward(torch.rand(1, g5[3], kw["crop_len"] + 1, device="cuda"))
     with pytest.raises(P.PkvValueError, match="B\\*N >= 2"):
         tr.forward(torch.rand(1, g5[3], 1, device="cuda"))
+
+
+def test_train_normalize_zero_rows_and_all_bypass(gpu):
+    """normalize_input on a window whose mean is 0 (clamp_min(·, 1e-12), mapper.cpp:288-291)
+    and the all-bypass pipeline (test_mapper.cpp:139-199's composition) against the
+    reference's tape."""
+    import torch
+    import paper_2605_16360_b200 as P
+    for kw in (dict(d_time=64, encoder_layers=1, encoder_heads=2, ffn_mult=2, d_head=8, crop_len=64, stride=32,
+                    normalize_input=1),
+               dict(d_time=32, encoder_layers=1, encoder_heads=2, ffn_mult=2, d_head=8, crop_len=64, stride=32,
+                    stage_conv=1, stage_encoder=1, stage_cross=1)):
+        g5 = (2, 3, 2, 2, 64)
+        pg, pc, og, oc = _cfgs(P, g5, kw)
+        rm = O.RefLib().mapper(og, oc, 9)
+        blob0 = rm.blob()
+        rng = np.random.default_rng(4)
+        x = rng.uniform(0.0, 2.0, (2, 2, 48)).astype(np.float32).astype(np.float64)
+        x[1, 0, :] = 0.0  # mean 0: the clamp's floor
+        dl = rng.normal(size=(2, 3, 48))
+        ref_logits, ref_grad = rm.train_grad(x, dl)
+        tr = P.MapperTrainer(pg, pc, blob0, ctx=gpu)
+        y = tr.forward(torch.from_numpy(x.astype(np.float32)).cuda()).cpu().numpy()
+        g = tr.backward(torch.from_numpy(dl).cuda()).cpu().numpy()
+        assert np.isfinite(y).all() and np.isfinite(g).all()
+        assert _rel(y.astype(np.float64), ref_logits) <= 5e-6
+        assert _rel(g, ref_grad) <= 2e-5
+
+
+def test_train_config_limits(gpu):
+    import paper_2605_16360_b200 as P
+    pg, pc, _, _ = _cfgs(P, (1, 33, 1, 2, 64), dict(d_time=32, encoder_layers=1, encoder_heads=2, ffn_mult=2,
+                                                   d_head=8, crop_len=64, stride=32))
+    tr = P.MapperTrainer(pg, pc, seed=1, ctx=gpu)
+    import torch
+    with pytest.raises(P.ConfigError, match="target_heads <= 32"):
+        tr.forward(torch.rand(1, 2, 16, device="cuda"))
