@@ -675,6 +675,9 @@ def main():
                     "frac": ach / tf_burst, "traffic": None, "peak_source": f"{src} bf16 burst (kernel timed alone)",
                     "note": "algorithmic FLOPs (2*d*Nq*Nk*Hq*L_s per pass); the pass is bounded by MUFU exp2 "
                             "throughput (16/clk/SM), not the tensor pipe (DESIGN.md section 5)"}
+            # informational: the kernel runs ~120 ms per launch at the power-capped clock the
+            # sustained figure was measured under
+            roof["frac_of_sustained"] = ach / tf_sus
         else:
             ach = work / (st[dom] * 1e-3) / 1e9
             roof = {"kernel": dom[:-3], "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
