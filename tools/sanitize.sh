@@ -21,3 +21,8 @@ echo "== memcheck: parity tests" >> "$OUT/sanitizer_memcheck.log"
 timeout 900 $CS --tool memcheck python -m pytest -q -x tests/test_pruner_gpu.py tests/test_score_gpu.py \
   tests/test_kernels_gpu.py tests/test_decode_gpu.py tests/test_select_f64_gpu.py >> "$OUT/sanitizer_memcheck.log" 2>&1
 echo "exit=$?" >> "$OUT/sanitizer_memcheck.log"
+# round 2 additions: GPU training, mapper precision mode 6 (e4m3 corrections), the streaming select
+echo "== memcheck: training / mode 6 / streaming select" >> "$OUT/sanitizer_memcheck.log"
+timeout 900 $CS --tool memcheck python -m pytest -q -x tests/test_train_gpu.py tests/test_select_compact_gpu.py \
+  "tests/test_mapper_gpu.py::test_fp16f8_mode_small_and_multiwindow" >> "$OUT/sanitizer_memcheck.log" 2>&1
+echo "exit=$?" >> "$OUT/sanitizer_memcheck.log"
