@@ -786,6 +786,8 @@ void Trainer::backward(const double* dlogits, double* grad, cudaStream_t st) {
     float* z = a("z");
     if (cfg.cross_active) {
         const size_t shm = (size_t)(2 * sd + hl * syn) * sizeof(float);
+        PKV_REQUIRE(shm <= 48 * 1024, PKV_ECONFIG, "mapper training: stage-3 backward needs synthetic_heads * d_head <= ",
+                    (48 * 1024 / 4 - hl * syn) / 2, ", got ", sd);
         stage3_back_kernel<<<(unsigned)R, (unsigned)(32 * hl), shm, st>>>(
             a("vals"), a("keys"), p("cross.queries"), p("cross.out.w"), a("attn"), a("heads"), a("dlogitT"), R,
             (int)hl, (int)syn, (int)dq, a("dvals"), a("dkeys"), gp("cross.queries"), gp("cross.out.w"),
