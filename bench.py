@@ -200,7 +200,7 @@ def max_over_ranks(v, world, dev):
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    t = torch.tensor([v], device=dev if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.item()
 
@@ -294,12 +294,20 @@ def run_ours(args, c, rank, world, local_rank):
     import torch
     import paper_2605_16360_b200 as P
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # test-only knobs (functional runs of the N > 1 path on a one-GPU box):
+    # PKV_BENCH_ONE_DEVICE=1 puts every rank on cuda:0, PKV_BENCH_BACKEND=gloo
+    # replaces NCCL for the timing collectives (layer sharding has no data-path collective)
+    dev_index = 0 if os.environ.get("PKV_BENCH_ONE_DEVICE") == "1" else local_rank
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-    ctx = P.Context(local_rank)
+        backend = os.environ.get("PKV_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    ctx = P.Context(dev_index)
     stream = torch.cuda.current_stream(dev)
     shard = args.shard if args.shard != "auto" else ("layer" if world > 1 else "none")
     # weak scaling replicas: an independent context per rank; sharded: every
@@ -312,7 +320,7 @@ def run_ours(args, c, rank, world, local_rank):
     barrier(world)
     torch.cuda.synchronize()
     l0 = ctx.launches()
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev_index) as clk:
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
