@@ -324,6 +324,12 @@ int64_t pkv_pruner_k(pkv_pruner p);
  *   kt, vt bf16/fp16 [L_l, H_l, N, dt] (target KV),
  *   k_out, v_out [L_l, H_l, K, dt], idx_out int32 [L_l, H_l, K] (nullable),
  *   scores_out fp32 [L_l, H_l, N] (nullable: mapped scores Ŷ). */
+/* Stage profiling of the next `runs` device-resident single-stream runs (pkv_pruner_run):
+ * CUDA events on the launching stream at the stage boundaries; pkv_pruner_profile_read
+ * synchronises and returns, per profiled run, the ms of {LSE pass, pooled pass, map,
+ * select, compaction} (ms_out [runs][5]). No reference counterpart (measurement). */
+pkv_status pkv_pruner_profile(pkv_pruner p, int64_t runs);
+pkv_status pkv_pruner_profile_read(pkv_pruner p, double* ms_out, int64_t cap_runs, int64_t* runs_out);
 pkv_status pkv_pruner_run(pkv_pruner p, const void* q_dev, const void* kp_dev, const void* kt_dev,
                           const void* vt_dev, void* k_out_dev, void* v_out_dev, int32_t* idx_out_dev,
                           float* scores_out_dev, void* stream);

@@ -96,6 +96,8 @@ SIGNATURES = {
     "pkv_pruner_run_two_device": (ctypes.c_int, [_c_vp] * 12),
     "pkv_pruner_run_lse": (ctypes.c_int, [_c_vp] * 11),
     "pkv_spearman": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i64, _c_vp, _c_vp]),
+    "pkv_pruner_profile": (ctypes.c_int, [_c_vp, _c_i64]),
+    "pkv_pruner_profile_read": (ctypes.c_int, [_c_vp, _c_vp, _c_i64, _c_i64p]),
     "pkv_trainer_create": (ctypes.c_int, [_c_vp, _c_i64p, _c_i64p, _c_vp, _c_i64, ctypes.POINTER(_c_vp)]),
     "pkv_trainer_destroy": (None, [_c_vp]),
     "pkv_trainer_param_count": (ctypes.c_int, [_c_vp, _c_i64p, _c_i64p]),

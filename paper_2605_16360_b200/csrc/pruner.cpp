@@ -37,6 +37,12 @@ struct pkv_pruner_s {
     static constexpr int kGroups = 8;   // target-layer groups of the map -> select -> compact -> D2H tail
     cudaEvent_t ev_in[kChunks + 2] = {};
     cudaEvent_t ev_grp[kGroups + 1] = {};
+    // stage profiling (pkv_pruner_profile): kProfEv events per run at the stage boundaries
+    // (LSE pass | pooled pass | map | select | compaction), recorded on the launching streams
+    static constexpr int kProfEv = 6;
+    std::vector<cudaEvent_t> prof_ev;
+    int64_t prof_max = 0, prof_next = 0;
+    cudaEvent_t prof(int i) const { return prof_ev[static_cast<size_t>(prof_next * kProfEv + i)]; }
     ~pkv_pruner_s() {
         if (ev) cudaEventDestroy(ev);
         if (ev_remote) cudaEventDestroy(ev_remote);
@@ -44,6 +50,7 @@ struct pkv_pruner_s {
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : ev_grp)
             if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
         if (copy_st) cudaStreamDestroy(copy_st);
     }
     int64_t slices() const { return (plan.t_hi - plan.t_lo) * (plan.h_hi - plan.h_lo); }
@@ -166,6 +173,10 @@ void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, con
                        ? static_cast<float*>(p->y_local.get(static_cast<size_t>(std::max<int64_t>(n_map, 1) * p->Hl * p->N) * 4))
                        : y_sel;
     int32_t* idx = idx_out ? idx_out : static_cast<int32_t*>(p->idx.get(static_cast<size_t>(slices * p->K) * 4));
+    // profiled run (device-resident, single-stream form only): boundary events
+    const bool prof = p->prof_next < p->prof_max && !arr && !lse_in && ps == ts && n_map > 0 && slices > 0 &&
+                      pl.mode != PKV_SHARD_HEAD;
+    if (prof) PKV_CUDA(cudaEventRecord(p->prof(0), ps));
     if (n_map > 0) {
         // (1) proxy scoring of this rank's proxy layers: X [L, H_s, N]
         const size_t q_off = static_cast<size_t>(pl.p_lo * p->Hq * p->N * p->dp) * 2;
@@ -183,7 +194,9 @@ void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, con
             count_launch(p->ctx, 2);
         } else if (!arr) {
             launch_score_lse(s, qp, kpp, nullptr, lam, ps, &p->score_aux);
+            if (prof) PKV_CUDA(cudaEventRecord(p->prof(1), ps));
             launch_score_pool(s, qp, kpp, lam, p->reduce_max, x, ps);
+            if (prof) PKV_CUDA(cudaEventRecord(p->prof(2), ps));
             count_launch(p->ctx, 2);
         } else {  // proxy layers scored chunk by chunk as their H2D copies land
             for (int c = 0; c < arr->chunks; ++c) {
@@ -210,6 +223,7 @@ void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, con
         // (2) mapper: Ŷ for target layers [a, b), all heads
         StageRange r_map("pkv.map");
         p->mapper->run(x, p->unit_off, p->N, p->out_unit, y_map, ps);
+        if (prof) PKV_CUDA(cudaEventRecord(p->prof(3), ps));
     }
     // (2b) head-group sharding: every mapped row to the owner of its head
     if (pl.mode == PKV_SHARD_HEAD) {
@@ -227,11 +241,16 @@ void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, con
     {
         StageRange r_sel("pkv.select");
         launch_topk_select(y_sel, slices, p->N, p->K, nullptr, idx, ts);
+        if (prof) PKV_CUDA(cudaEventRecord(p->prof(4), ts));
     }
     // (4) packed KV gather
     StageRange r_cmp("pkv.compact");
     launch_compact_kv(kt, vt, idx, slices, p->N, p->K, p->dt * 2, k_out, v_out, p->ctx->sm_count, ts);
     count_launch(p->ctx, 2);
+    if (prof) {
+        PKV_CUDA(cudaEventRecord(p->prof(5), ts));
+        ++p->prof_next;
+    }
 }
 
 }  // namespace
@@ -260,6 +279,37 @@ pkv_status pkv_pruner_run(pkv_pruner p, const void* q, const void* kp, const voi
         PKV_REQUIRE_VALUE(p != nullptr, "null pkv_pruner");
         auto st = static_cast<cudaStream_t>(stream);
         run_pruner(p, q, kp, kt, vt, k_out, v_out, idx_out, scores_out, st, st);
+    });
+}
+
+pkv_status pkv_pruner_profile(pkv_pruner p, int64_t runs) {
+    return guard([&] {
+        PKV_REQUIRE_VALUE(p && runs >= 0, "pkv_pruner_profile: runs must be >= 0");
+        const size_t need = static_cast<size_t>(runs * pkv_pruner_s::kProfEv);
+        while (p->prof_ev.size() < need) {
+            cudaEvent_t e = nullptr;
+            PKV_CUDA(cudaEventCreate(&e));
+            p->prof_ev.push_back(e);
+        }
+        p->prof_max = runs;
+        p->prof_next = 0;
+    });
+}
+
+pkv_status pkv_pruner_profile_read(pkv_pruner p, double* ms_out, int64_t cap_runs, int64_t* runs_out) {
+    return guard([&] {
+        PKV_REQUIRE_VALUE(p, "null pruner");
+        const int64_t n = std::min(p->prof_next, cap_runs);
+        for (int64_t r = 0; r < n; ++r) {
+            const size_t b = static_cast<size_t>(r * pkv_pruner_s::kProfEv);
+            PKV_CUDA(cudaEventSynchronize(p->prof_ev[b + pkv_pruner_s::kProfEv - 1]));
+            for (int i = 0; i + 1 < pkv_pruner_s::kProfEv; ++i) {
+                float ms = 0.0f;
+                PKV_CUDA(cudaEventElapsedTime(&ms, p->prof_ev[b + i], p->prof_ev[b + i + 1]));
+                ms_out[r * (pkv_pruner_s::kProfEv - 1) + i] = ms;
+            }
+        }
+        *runs_out = n;
     });
 }
 

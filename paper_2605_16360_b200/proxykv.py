@@ -797,6 +797,18 @@ class Pruner:
             _lib._lib.pkv_pruner_destroy(h)
             self.h = None
 
+    def profile(self, runs: int):
+        """Record stage-boundary CUDA events during the next `runs` device-resident runs."""
+        check(lib().pkv_pruner_profile(self.h, int(runs)))
+
+    def profile_read(self):
+        """Per profiled run: ms of (LSE pass, pooled pass, map, select, compaction)."""
+        cap = 4096
+        buf = (ctypes.c_double * (cap * 5))()
+        n = ctypes.c_int64()
+        check(lib().pkv_pruner_profile_read(self.h, buf, cap, ctypes.byref(n)))
+        return [tuple(buf[r * 5:(r + 1) * 5]) for r in range(n.value)]
+
     def run(self, q, kp, kt, vt, k_out, v_out, idx_out=None, scores_out=None, stream=None):
         check(lib().pkv_pruner_run(self.h, _ptr(q), _ptr(kp), _ptr(kt), _ptr(vt), _ptr(k_out), _ptr(v_out),
                                    _ptr(idx_out), _ptr(scores_out), _stream(stream)))
