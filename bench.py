@@ -354,7 +354,12 @@ def run_ours(args, c, rank, world, local_rank):
     del arm
     torch.cuda.empty_cache()
     if (world > 1 and not args.no_extras) or args.extras:
-        # the extra legs never cost the main line: a leg that raises is reported, not fatal
+        # the extra legs never cost the main line: a leg that raises is reported, not fatal, and a
+        # watchdog emits the line without them if they have not finished within EXTRAS_BUDGET_S
+        partial = dict(result)
+        dog = threading.Timer(EXTRAS_BUDGET_S, extras_timeout, args=(partial, args, c, world, rank))
+        dog.daemon = True
+        dog.start()
         for key, leg in (("weak_scaling", lambda: weak_scaling(P, ctx, c, dev, world, rank, args, stream)),
                          ("sharded_configs", lambda: sharded_configs(P, ctx, dev, world, rank, args, stream))):
             try:
@@ -362,10 +367,27 @@ def run_ours(args, c, rank, world, local_rank):
             except Exception as exc:  # noqa: BLE001
                 result[key] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
                 torch.cuda.synchronize()
+        dog.cancel()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
     return result
+
+
+EXTRAS_BUDGET_S = float(os.environ.get("PKV_BENCH_EXTRAS_BUDGET_S", "420"))
+
+
+def extras_timeout(partial, args, c, world, rank):
+    """The extra legs overran (e.g. a communicator that never forms): rank 0 emits the
+    main line with the legs marked, and every rank exits."""
+    if rank == 0:
+        for key in ("weak_scaling", "sharded_configs"):
+            partial.setdefault(key, {"error": f"not finished within {EXTRAS_BUDGET_S:.0f} s"})
+        try:
+            emit(build_line(partial, args, c, world))
+        finally:
+            os._exit(0)
+    os._exit(0)
 
 
 def weak_scaling(P, ctx, c, dev, world, rank, args, stream):
@@ -615,6 +637,27 @@ def run_reference(args, c):
 
 
 # -------------------------------------------------------------------- main --
+_OUT_FD = 1  # the real stdout (main() routes fd 1 to stderr for native output)
+
+
+def emit(obj):
+    os.write(_OUT_FD, (json.dumps(obj) + "\n").encode())
+
+
+def cpu_baseline_entry(c):
+    """The reference's CPU path on the host cores, a bounded sample (world 1 only)."""
+    try:
+        threads = os.cpu_count() or 1
+        stc = cpu_reference_sample(c, threads)
+        sec = sum(stc.values())
+        return {"cpu_baseline": {"value": c["N"] / sec, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(),
+                                 "kind": "reference", "sample": cpu_sample_desc(c, threads), "extrapolated": True,
+                                 "stage_s": {k: round(v, 3) for k, v in stc.items()},
+                                 "legs": cpu_legs(c, stc, threads)}}
+    except Exception as e:  # noqa: BLE001
+        return {"cpu_baseline": {"value": None, "unavailable": f"{type(e).__name__}: {e}"}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -644,11 +687,9 @@ def main():
     # version banner and INFO log, CUDA libraries) goes to stderr, the line to the
     # saved stdout descriptor
     sys.stdout.flush()
-    out_fd = os.dup(1)
+    global _OUT_FD
+    _OUT_FD = os.dup(1)
     os.dup2(2, 1)
-
-    def emit(obj):
-        os.write(out_fd, (json.dumps(obj) + "\n").encode())
 
     if args.impl == "reference":
         if rank == 0:
@@ -661,6 +702,14 @@ def main():
     r = run_ours(args, c, rank, world, local_rank)
     if rank != 0:
         return
+    line = build_line(r, args, c, world)
+    if not args.no_cpu_baseline and world == 1:
+        line.update(cpu_baseline_entry(c))
+    emit(line)
+
+
+def build_line(r, args, c, world):
+    """The JSON line (without the CPU baseline) from run_ours' result."""
     hbm, tf_burst, tf_sus, src = peaks()
     ms = r["ms"]
     sharded = r["shard"] != "none"
@@ -762,18 +811,8 @@ def main():
                        "h2d_bytes_per_step": e["h2d"], "d2h_bytes_per_step": e["d2h"], "ms_per_step": e["ms"],
                        "note": "pkv_pruner_run_host on every rank at once (wall clock, synchronised per call, max over "
                                "ranks); bytes are rank 0's"}
-    if not args.no_cpu_baseline and world == 1:
-        try:
-            threads = os.cpu_count() or 1
-            stc = cpu_reference_sample(c, threads)
-            sec = sum(stc.values())
-            line["cpu_baseline"] = {"value": c["N"] / sec, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(),
-                                    "kind": "reference", "sample": cpu_sample_desc(c, threads), "extrapolated": True,
-                                    "stage_s": {k: round(v, 3) for k, v in stc.items()},
-                                    "legs": cpu_legs(c, stc, threads)}
-        except Exception as e:  # noqa: BLE001
-            line["cpu_baseline"] = {"value": None, "unavailable": f"{type(e).__name__}: {e}"}
-    emit(line)
+    return line
+
 
 
 if __name__ == "__main__":
