@@ -316,15 +316,13 @@ __global__ void __launch_bounds__(P1<D>::kThreads, 1)
             }
             const uint32_t base = tmem + ((quad * 32) << 16) + sb * C::kBK + seg * C::kSegCols;
             uint32_t ra[32], rb[32];
-            tmem_ld32(base, ra);
-            tmem_ld32(base + 32, rb);
+            tmem_ld64(base, ra, rb);
             tmem_ld_wait();
 #pragma unroll
             for (int c = 0; c < kChunks; ++c) {
                 uint32_t na[32], nb[32];
                 if (c + 1 < kChunks) {  // prefetch the next 64 columns while this chunk computes
-                    tmem_ld32(base + 64 * (c + 1), na);
-                    tmem_ld32(base + 64 * (c + 1) + 32, nb);
+                    tmem_ld64(base + 64 * (c + 1), na, nb);  // one MIO op (shared with MUFU) per chunk
                 } else {
                     tc_fence_before();
                     __syncwarp();
