@@ -35,7 +35,9 @@ struct pkv_pruner_s {
     cudaStream_t copy_st = nullptr;
     static constexpr int kChunks = 16;  // proxy-layer chunks of the H2D
     static constexpr int kGroups = 8;   // target-layer groups of the map -> select -> compact -> D2H tail
+    static constexpr int kSub = 4;      // KV-head groups of the first chunk (its copy is the exposed one)
     cudaEvent_t ev_in[kChunks + 2] = {};
+    cudaEvent_t ev_sub[kSub] = {};
     cudaEvent_t ev_grp[kGroups + 1] = {};
     // stage profiling (pkv_pruner_profile): kProfEv events per run at the stage boundaries
     // (LSE pass | pooled pass | map | select | compaction), recorded on the launching streams
@@ -49,6 +51,8 @@ struct pkv_pruner_s {
         for (cudaEvent_t e : ev_in)
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : ev_grp)
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : ev_sub)
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
         if (copy_st) cudaStreamDestroy(copy_st);
@@ -64,6 +68,11 @@ struct HostArrival {
     int chunks = 0;
     int64_t chunk_layers = 0;
     const cudaEvent_t* ev_chunk = nullptr;
+    // chunk 0 (one proxy layer) split into `sub` KV-head groups, each scored as
+    // soon as its own copy lands (ev_sub[s]): only the first group's copy is
+    // exposed before the GPU starts
+    int sub = 1;
+    const cudaEvent_t* ev_sub = nullptr;
     cudaEvent_t ev_kv = nullptr;
     // outputs leaving for the host: when set (layer mode), the tail runs per
     // target-layer group and each group's packed K/V + indices are copied out
@@ -202,6 +211,24 @@ void run_pruner(pkv_pruner p, const void* q, const void* kp, const void* kt, con
             for (int c = 0; c < arr->chunks; ++c) {
                 const int64_t l0 = c * arr->chunk_layers, l1 = std::min<int64_t>(s.L, l0 + arr->chunk_layers);
                 if (l0 >= l1) break;
+                if (c == 0 && arr->sub > 1 && l1 - l0 == 1) {  // the first layer, per KV-head group
+                    const int64_t g = s.Hq / s.Hkv, hk = s.Hkv / arr->sub;
+                    for (int sg = 0; sg < arr->sub; ++sg) {
+                        const int64_t k0 = sg * hk;
+                        ScoreShape sc = s;
+                        sc.L = 1;
+                        sc.Hq = hk * g;
+                        sc.Hkv = hk;
+                        PKV_CUDA(cudaStreamWaitEvent(ps, arr->ev_sub[sg], 0));
+                        const auto* qc = qp + static_cast<size_t>(k0 * g * p->N * p->dp) * 2;
+                        const auto* kc = kpp + static_cast<size_t>(k0 * p->N * p->dp) * 2;
+                        __nv_bfloat16* lc = lam + static_cast<size_t>(k0 * g * s.Nq) * 8;
+                        launch_score_lse(sc, qc, kc, nullptr, lc, ps, &p->score_aux);
+                        launch_score_pool(sc, qc, kc, lc, p->reduce_max, x + static_cast<size_t>(k0 * s.Nk), ps);
+                        count_launch(p->ctx, 2);
+                    }
+                    continue;
+                }
                 ScoreShape sc = s;
                 sc.L = l1 - l0;
                 PKV_CUDA(cudaStreamWaitEvent(ps, arr->ev_chunk[c], 0));
@@ -412,6 +439,7 @@ pkv_status pkv_pruner_run_host(pkv_pruner p, const void* q_h, const void* kp_h, 
             PKV_CUDA(cudaStreamCreateWithFlags(&p->copy_st, cudaStreamNonBlocking));
             for (cudaEvent_t& e : p->ev_in) PKV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             for (cudaEvent_t& e : p->ev_grp) PKV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            for (cudaEvent_t& e : p->ev_sub) PKV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         }
         cudaStream_t cs = p->copy_st;
         constexpr int kC = pkv_pruner_s::kChunks;
@@ -426,10 +454,26 @@ pkv_status pkv_pruner_run_host(pkv_pruner p, const void* q_h, const void* kp_h, 
         arr.chunk_layers = std::max<int64_t>(1, (nl + kC - 1) / kC);
         arr.chunks = kC;
         arr.ev_chunk = p->ev_in;
+        constexpr int kS = pkv_pruner_s::kSub;
+        if (arr.chunk_layers == 1 && nl > 0 && Hs % kS == 0) {
+            arr.sub = kS;
+            arr.ev_sub = p->ev_sub;
+        }
         for (int c = 0; c < kC; ++c) {
             const int64_t l0 = pl.p_lo + c * arr.chunk_layers;
             const int64_t l1 = std::min<int64_t>(pl.p_lo + nl, l0 + arr.chunk_layers);
-            if (l0 < l1) {
+            if (c == 0 && arr.sub > 1 && l0 < l1) {  // first layer per KV-head group (Q heads of the group + its K head)
+                const size_t qg = q_layer / kS, kg = kp_layer / kS;
+                for (int sg = 0; sg < kS; ++sg) {
+                    PKV_CUDA(cudaMemcpyAsync(in + l0 * q_layer + sg * qg,
+                                             static_cast<const uint8_t*>(q_h) + l0 * q_layer + sg * qg, qg,
+                                             cudaMemcpyHostToDevice, cs));
+                    PKV_CUDA(cudaMemcpyAsync(in + qb + l0 * kp_layer + sg * kg,
+                                             static_cast<const uint8_t*>(kp_h) + l0 * kp_layer + sg * kg, kg,
+                                             cudaMemcpyHostToDevice, cs));
+                    PKV_CUDA(cudaEventRecord(p->ev_sub[sg], cs));
+                }
+            } else if (l0 < l1) {
                 PKV_CUDA(cudaMemcpyAsync(in + l0 * q_layer, static_cast<const uint8_t*>(q_h) + l0 * q_layer,
                                          (l1 - l0) * q_layer, cudaMemcpyHostToDevice, cs));
                 PKV_CUDA(cudaMemcpyAsync(in + qb + l0 * kp_layer, static_cast<const uint8_t*>(kp_h) + l0 * kp_layer,

@@ -121,15 +121,16 @@ def test_pruner_deterministic(tiny):
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
 
 
-@pytest.mark.parametrize("Ls,Ll,Hl", [(5, 7, 2), (16, 32, 2), (3, 3, 4)])
-def test_pruner_host_grouped_tail_matches_device(gpu, Ls, Ll, Hl):
+@pytest.mark.parametrize("Ls,Ll,Hl,Hq,Hs", [(5, 7, 2, 4, 2), (16, 32, 2, 4, 2), (3, 3, 4, 4, 2), (4, 8, 2, 16, 8)])
+def test_pruner_host_grouped_tail_matches_device(gpu, Ls, Ll, Hl, Hq, Hs):
     """pkv_pruner_run_host maps / selects / compacts per target-layer group and
     copies each group out while the next is mapped; the result must equal the
     device-resident run bit for bit, for unit counts that do not split evenly
-    into the groups and pairings that are not 2:1."""
+    into the groups and pairings that are not 2:1. H_s = 8: the first proxy
+    layer arrives and is scored in 4 KV-head groups (GQA 2)."""
     import torch
     import paper_2605_16360_b200 as P
-    Hq, Hs, dp, dt, N, rho = 4, 2, 64, 64, 1024, 0.3
+    dp, dt, N, rho = 64, 64, 1024, 0.3
     geom = P.ModelGeometry(Ll, Hl, Ls, Hs, dt)
     m = P.Mapper(geom, P.MapperConfig(encoder_layers=1), seed=3, ctx=gpu)
     pr = P.Pruner(m, Hq, dp, dt, N, rho)
