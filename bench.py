@@ -462,7 +462,11 @@ def stage_breakdown(P, ctx, arm, c, stream, args):
     out["map_ms"] = time_loop(map_call, it, stream)
     # the short stages: an untimed loop first and long timed loops — the first few ms of
     # back-to-back launches after the long stages run ~45 % slow for select
-    # (tools/probe_select_bench.py: 56.8 then 37.0 us on the same data; ncu: 39 us per launch)
+    # (tools/probe_select_bench.py: 56.8 then 37.0 us on the same data; ncu: 39 us per launch):
+    # the power-capped clock after the long stages; an idle gap lets it recover before these
+    # latency-bound kernels are timed alone (their in-step cost is stages_live_ms)
+    torch.cuda.synchronize()
+    time.sleep(0.5)
     time_loop(sel_call, 100, stream)
     out["select_ms"] = time_loop(sel_call, 200, stream)
     time_loop(cmp_call, 20, stream)
@@ -779,7 +783,8 @@ def build_line(r, args, c, world):
                                         "recorded on the launching stream at the stage boundaries "
                                         "(pkv_pruner_profile); the LSE pass includes its max|k| / flag setup")
         line["stages_note"] = ("each stage alone through the C ABI with preallocated outputs, back-to-back launches "
-                               "queued behind a spin kernel (device time, not host launch overhead)")
+                               "queued behind a spin kernel (device time, not host launch overhead); select and "
+                               "compact after a 0.5 s idle gap so the power-capped clock has recovered")
         fc = 2 * c["dp"] * (c["N"] * (c["N"] + 1) // 2) * c["Hq"] * c["Ls"]  # causal pairs
         line["scoring_single_pass"] = {
             "note": "causal scoring with the LSE from the proxy's prefill attention (pkv_proxy_prefill_attention, "
