@@ -146,7 +146,12 @@ def test_compaction_bit_exact(gpu, S, n, k, d, dtype):
 @pytest.mark.parametrize("S,n,rho,d,kind", [(256, 32768, 0.2, 128, "uniform"), (16, 20000, 0.1, 64, "ties"),
                                             (3, 8193, 0.5, 128, "allequal"), (5, 4099, 0.3, 64, "signed0"),
                                             (2, 170000, 0.2, 128, "logits"), (4, 1000, 0.2, 64, "uniform"),
-                                            (9, 16387, 0.37, 8, "ties")])
+                                            (9, 16387, 0.37, 8, "ties"),
+                                            # budget-sweep rows, one slice per co-resident CTA and beyond
+                                            (256, 8192, 0.1, 128, "uniform"), (256, 16384, 0.1, 128, "logits"),
+                                            (296, 4096, 0.5, 128, "ties"), (7, 100, 1.0, 16, "uniform"),
+                                            (40, 3000, 0.01, 24, "signed0"),
+                                            (600, 2048, 0.2, 64, "uniform")])
 def test_select_compact(gpu, S, n, rho, d, kind):
     """pkv_select_compact == oracle select + oracle gather, bit for bit (indices and packed rows)."""
     import torch
@@ -193,3 +198,31 @@ def test_repeated_calls_and_offset_views(gpu):
         omask, oidx = O.topk_select(s, k)
         np.testing.assert_array_equal(mask.cpu().numpy(), omask)
         np.testing.assert_array_equal(idx.cpu().numpy(), oidx)
+
+
+def test_select_compact_two_streams_repeated(gpu):
+    """pkv_select_compact called many times on two streams with changing geometry
+    (register-cached and streaming selects, several row widths): every call vs the oracle."""
+    import torch
+    import paper_2605_16360_b200 as P
+    r = np.random.RandomState(11)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    for it, (S, n, d) in enumerate([(64, 8192, 128), (256, 4096, 64), (3, 16384, 128), (64, 8192, 128),
+                                    (128, 12000, 8), (256, 4096, 64)] * 2):
+        s = r.uniform(0, 1, (S, n)).astype(np.float32)
+        k = O.retention_count(0.1 + 0.07 * (it % 6), n)
+        st = streams[it % 2]
+        with torch.cuda.stream(st):
+            sc = torch.from_numpy(s).to("cuda", non_blocking=False)
+            kin = torch.randint(-(1 << 15), 1 << 15, (S, n, d), device="cuda", dtype=torch.int32).to(torch.int16)
+            vin = torch.randint(-(1 << 15), 1 << 15, (S, n, d), device="cuda", dtype=torch.int32).to(torch.int16)
+            idx, ko, vo = P.select_compact(sc, kin, vin, k, ctx=gpu, stream=st)
+        outs.append((s, k, kin, vin, idx, ko, vo, st))
+    torch.cuda.synchronize()
+    for s, k, kin, vin, idx, ko, vo, st in outs:
+        _, oidx = O.topk_select(s, k)
+        np.testing.assert_array_equal(idx.cpu().numpy(), oidx)
+        eko, evo = O.compact_kv(kin.cpu().numpy().view(np.uint16), vin.cpu().numpy().view(np.uint16), oidx)
+        np.testing.assert_array_equal(ko.cpu().numpy().view(np.uint16), eko)
+        np.testing.assert_array_equal(vo.cpu().numpy().view(np.uint16), evo)

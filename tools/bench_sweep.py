@@ -55,8 +55,14 @@ for N in (8192, 16384, 32768, 65536, 131072):
         for _ in range(3):
             sel()
             cmp()
+        unit = lambda: P.check(L.pkv_select_compact(ctx.h, scores.data_ptr(), S, N, K, kt.data_ptr(), vt.data_ptr(),
+                                                     dt, 2, idx.data_ptr(), ko.data_ptr(), vo.data_ptr(),
+                                                     st.cuda_stream))
+        for _ in range(3):
+            unit()
         t_sel = bench.time_loop(sel, 20, st)
         t_cmp = bench.time_loop(cmp, 10, st)
+        t_sc = bench.time_loop(unit, 10, st)  # pkv_select_compact: both kernels as one call
         alt = {}
         for mode, name in ((0, "register_cached_radix"), (1, "streaming")):
             prev = path(mode)  # force one select kernel (select.cu / select_stream.cu)
@@ -68,12 +74,14 @@ for N in (8192, 16384, 32768, 65536, 131072):
         r = dict(N=N, rho=rho, K=K, select_ms=t_sel, compact_ms=t_cmp,
                  select_kernel_ms=alt,
                  select_gbs=b_sel / t_sel / 1e6, compact_gbs=b_cmp / t_cmp / 1e6,
-                 combined_frac_hbm=(b_sel + b_cmp) / (t_sel + t_cmp) / 1e6 / hbm)
+                 combined_frac_hbm=(b_sel + b_cmp) / (t_sel + t_cmp) / 1e6 / hbm,
+                 select_compact_ms=t_sc, select_compact_frac_hbm=(b_sel + b_cmp) / t_sc / 1e6 / hbm)
         rows.append(r)
         print(f"N={N:6d} rho={rho:.1f} K={K:6d}  select {t_sel * 1e3:6.1f} us (cached radix "
               f"{alt['register_cached_radix'] * 1e3:6.1f}, streaming {alt['streaming'] * 1e3:6.1f}) "
               f"{r['select_gbs']:5.0f} GB/s  compact {t_cmp:6.3f} ms {r['compact_gbs']:5.0f} GB/s  "
-              f"select+compact {100 * r['combined_frac_hbm']:.1f}% of {hbm:.0f} GB/s", flush=True)
+              f"select+compact {100 * r['combined_frac_hbm']:.1f}% of {hbm:.0f} GB/s; pkv_select_compact "
+              f"{t_sc * 1e3:6.1f} us {100 * r['select_compact_frac_hbm']:.1f}%", flush=True)
         del ko, vo, idx
     del scores, kt, vt
     torch.cuda.empty_cache()
