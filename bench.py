@@ -84,6 +84,17 @@ def flops_mapper(c, D=512, enc=6, Dh=64):
     return unique_pairs(c["Ll"], c["Ls"]) * windows(c["N"]) * per
 
 
+def mma_flops_mapper(c, planes=3, D=512, enc=6, Dh=64):
+    """Tensor-core work the mapper issues in a split-precision mode: its GEMM-shaped
+    products (conv stem, QKV / Wo / FFN, stage-3 projections) run as `planes` MMAs
+    each (3 in FP16X3, mode 3), the encoder attention's QK^T and PV as one."""
+    nw = min(c["N"], 2048)
+    syn = c["Hs"]
+    gemm = (2 * nw * 256 * c["Hs"] * 3 + 2 * nw * 512 * 768 + enc * 24 * nw * D * D + 4 * nw * D * syn * Dh)
+    rest = enc * 4 * nw * nw * D + 4 * nw * c["Hl"] * syn * Dh + 2 * nw * c["Hl"] * Dh
+    return unique_pairs(c["Ll"], c["Ls"]) * windows(c["N"]) * (planes * gemm + rest)
+
+
 def k_of(c):
     return math.ceil(c["rho"] * c["N"])
 
@@ -797,7 +808,12 @@ def build_line(r, args, c, world):
         line["stage_roofline"] = {
             "score_lse": {"TFLOP/s": flops_score_pass(c) / st["score_lse_ms"] / 1e9},
             "score_pool": {"TFLOP/s": flops_score_pass(c) / st["score_pool_ms"] / 1e9},
-            "map": {"TFLOP/s": flops_mapper(c) / st["map_ms"] / 1e9},
+            "map": {"TFLOP/s": flops_mapper(c) / st["map_ms"] / 1e9,
+                    **({"mma_issued_TFLOP/s": mma_flops_mapper(c) / st["map_ms"] / 1e9,
+                        "mma_issued_frac_of_burst": mma_flops_mapper(c) / st["map_ms"] / 1e9 / tf_burst,
+                        "note": "FP16X3: each GEMM-shaped product issued as 3 fp16 MMAs (hi/lo planes), the "
+                                "attention as 1; TFLOP/s above is the reference mapper's algorithmic work"}
+                       if args.precision == 3 else {})},
             "select": {"GB/s": bytes_select(c) / st["select_ms"] / 1e6,
                        "frac_hbm": bytes_select(c) / st["select_ms"] / 1e6 / hbm},
             "compact": {"GB/s": bytes_compact(c) / st["compact_ms"] / 1e6,
