@@ -32,13 +32,16 @@ FIX = os.path.join(ROOT, "gpurun_in", "fullsize_qwen3_64k")
 
 @pytest.mark.skipif(not os.path.exists(os.path.join(FIX, "oracle_y_f32.npy")),
                     reason="oracle fixture not shipped (tools/fullsize_oracle_cfg.py)")
-def test_fullsize_qwen3_64k_all_slices(gpu):
+@pytest.mark.parametrize("prec", [3, 6])
+def test_fullsize_qwen3_64k_all_slices(gpu, prec):
+    """prec 3 (FP16X3, the default) must hold the bars; prec 6 (e4m3 corrections) is
+    measured for the precision table and held to the rel bar only."""
     import torch
     import bench
     import paper_2605_16360_b200 as P
     c = bench.CONFIGS["qwen3_64k"]
     geom = P.ModelGeometry(c["Ll"], c["Hl"], c["Ls"], c["Hs"], c["dt"])
-    m = P.Mapper(geom, P.MapperConfig(), seed=7, ctx=gpu)
+    m = P.Mapper(geom, P.MapperConfig(), seed=7, precision=prec, ctx=gpu)
     pr = P.Pruner(m, c["Hq"], c["dp"], c["dt"], c["N"], c["rho"])
     q, kp, kt, vt = bench.make_inputs(c, torch.device("cuda"), 1234)
     K = pr.k
@@ -67,11 +70,12 @@ def test_fullsize_qwen3_64k_all_slices(gpu):
         om, _ = O.topk_select(w, K)
         ov.append(O.topk_overlap_per_slice(mask_g[ll - 1], om, K))
     rel, ov = np.concatenate(rel), np.concatenate(ov)
-    line = (f"qwen3_64k: {rel.size} slices; mapped-score norm-rel max {rel.max():.2e} mean {rel.mean():.2e}; "
-            f"Top-K overlap mean {ov.mean():.5f} min {ov.min():.5f}; slices below 0.999: {(ov < 0.999).sum()}")
+    line = (f"qwen3_64k mapper precision {prec}: {rel.size} slices; mapped-score norm-rel max {rel.max():.2e} "
+            f"mean {rel.mean():.2e}; Top-K overlap mean {ov.mean():.5f} min {ov.min():.5f}; slices below 0.999: {(ov < 0.999).sum()}")
     print(line)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", "fullsize_qwen3_64k_summary.txt"), "w") as f:
+    with open(os.path.join(ROOT, "gpurun_out", "fullsize_qwen3_64k_summary.txt"), "a") as f:
         f.write(line + "\n")
     assert rel.max() <= 1e-3
-    assert ov.mean() >= 0.999
+    if prec == 3:
+        assert ov.mean() >= 0.999
